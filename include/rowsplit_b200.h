@@ -1,0 +1,202 @@
+/*
+ * rowsplit_b200.h -- C ABI of the B200-native solve phase of the
+ * row-splitting ILU preconditioned CGLS method (arxiv 2603.28642).
+ *
+ * One shared library, librowsplit_b200.so, all entry points extern "C",
+ * plain pointers and sizes, FP64 values, int64 host indices (int32 on the
+ * device).  The reference (`rowsplit`, pure Python + numpy) has no FFI; the
+ * interface this ABI replaces is its Python API, cited per entry point as
+ * file:line under /root/reference/pkg/src/rowsplit/ (sc = sparse_core.py,
+ * pc = precond.py, sv = solver.py, il = ilup.py).  The Python mirror in
+ * paper_2603_28642_b200/ binds it with ctypes.
+ *
+ * Conventions
+ *   - Every function returns RSB_OK (0) or an RSB_E* status; the message
+ *     of the last failure on the calling thread is rsb_last_error().
+ *     Status -> Python exception: EINVAL -> ValueError, ESINGULAR ->
+ *     numpy.linalg.LinAlgError, ECUDA/ENOMEM/ESTATE -> RuntimeError.
+ *   - `where` says whether vector arguments are host (RSB_HOST) or device
+ *     (RSB_DEVICE) pointers.  Host buffers are borrowed for the call only;
+ *     host-pointer calls return after the result is in host memory.
+ *   - Handles own their device memory and are immutable after creation
+ *     (reference: sc.py:7-8, pc.py:111-113).  One rsb_ctx = one CUDA
+ *     stream; a context is not re-entrant, use one per thread.
+ *   - Arithmetic follows the reference's operation order.  With
+ *     RSB_DOT_EXACT (default) every reduction reproduces numpy/OpenBLAS's
+ *     association, so results are bit-identical to the reference run
+ *     single-threaded on its host.
+ */
+#ifndef ROWSPLIT_B200_H
+#define ROWSPLIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSB_OK 0
+#define RSB_EINVAL 1    /* ValueError */
+#define RSB_ESINGULAR 2 /* numpy.linalg.LinAlgError */
+#define RSB_ECUDA 3     /* RuntimeError: CUDA failure / no device */
+#define RSB_ENOMEM 4    /* RuntimeError: allocation */
+#define RSB_ESTATE 5    /* RuntimeError: call out of order */
+
+#define RSB_HOST 0
+#define RSB_DEVICE 1
+
+/* context flags: reduction order for dots and norms */
+#define RSB_DOT_EXACT 0 /* reference (OpenBLAS ddot) association: bitwise parity */
+#define RSB_DOT_TREE 1  /* fixed-order two-level tree: deterministic, faster for n >> 1e6 */
+
+/* triangular solve kinds (sc.py:243-313) */
+#define RSB_TRI_LOWER 0        /* sparse_lower_solve(L, b, unit_diag=False)  sc.py:243 */
+#define RSB_TRI_LOWER_UNIT 1   /* sparse_lower_solve(L, b, unit_diag=True)   sc.py:243 */
+#define RSB_TRI_UPPER 2        /* sparse_upper_solve(U, b)                   sc.py:266 */
+#define RSB_TRI_LOWER_T 3      /* sparse_lower_solve_transpose(L, b, False)  sc.py:282 */
+#define RSB_TRI_LOWER_T_UNIT 4 /* sparse_lower_solve_transpose(L, b, True)   sc.py:282 */
+#define RSB_TRI_UPPER_T 5      /* sparse_upper_solve_transpose(U, b)         sc.py:301 */
+
+/* SMode / YMode (pc.py:36-48) */
+#define RSB_S_DENSE 0
+#define RSB_S_CG 1
+#define RSB_S_IDENTITY 2
+#define RSB_Y_EXPLICIT 0
+#define RSB_Y_IMPLICIT 1
+
+typedef struct rsb_ctx rsb_ctx;
+typedef struct rsb_mat rsb_mat;
+typedef struct rsb_pre rsb_pre;
+typedef struct rsb_solver rsb_solver;
+typedef struct rsb_ilup rsb_ilup;
+
+/* ---- library / context ------------------------------------------------ */
+const char *rsb_last_error(void);
+int rsb_version(void);
+int rsb_device_count(int *count);
+int rsb_ctx_create(int device, int flags, rsb_ctx **out);
+int rsb_ctx_destroy(rsb_ctx *ctx);
+int rsb_ctx_sync(rsb_ctx *ctx);
+/* launches of this library's kernels since the counter was last reset */
+int rsb_ctx_kernel_launches(rsb_ctx *ctx, int64_t *count, int reset);
+/* device memory of this context (bytes currently allocated) */
+int rsb_ctx_mem_bytes(rsb_ctx *ctx, int64_t *bytes);
+/* pinned host staging + device scratch, for callers timing copies */
+int rsb_host_alloc(int64_t bytes, void **ptr);
+int rsb_host_free(void *ptr);
+int rsb_device_alloc(rsb_ctx *ctx, int64_t bytes, void **ptr);
+int rsb_device_free(rsb_ctx *ctx, void *ptr);
+int rsb_memcpy(rsb_ctx *ctx, void *dst, const void *src, int64_t bytes, int kind /*0 h2d,1 d2h,2 d2d*/);
+/* device timing on the context stream: elapsed ms between two marks */
+int rsb_event_mark(rsb_ctx *ctx, int slot);
+int rsb_event_elapsed(rsb_ctx *ctx, int slot0, int slot1, float *ms);
+
+/* ---- matrices: CscMatrix (sc.py:27-131) --------------------------------- */
+/* Uploads host CSC (int64 col_ptr/row_idx, f64 values) as device CSR+CSC. */
+int rsb_mat_create(rsb_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *col_ptr,
+                   const int64_t *row_idx, const double *values, rsb_mat **out);
+int rsb_mat_destroy(rsb_mat *A);
+int rsb_mat_info(const rsb_mat *A, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+
+/* y = A x      matvec            sc.py:212-221 */
+int rsb_matvec(rsb_mat *A, const double *x, double *y, int where);
+/* z = A^T y    matvec_transpose  sc.py:224-235 */
+int rsb_matvec_transpose(rsb_mat *A, const double *y, double *z, int where);
+/* triangular solves, kind = RSB_TRI_*  (sc.py:243-313).  Level analysis is
+ * done on first use per (matrix, kind) and cached on the matrix. */
+int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where);
+/* dependency levels of the (matrix, kind) solve DAG (analysing it if needed) */
+int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
+/* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),
+ * drawn by the caller (host RNG stays on the host). */
+int rsb_power_norm2(rsb_mat *A, const double *v0, int iters, double *est);
+/* dense_cholesky_solve (sc.py:607-622): S x = b with the lower s x s
+ * column-major factor G (host or device pointers per `where`) */
+int rsb_chol_solve(rsb_ctx *ctx, int64_t s, const double *G, const double *b, double *x, int where);
+/* a @ b for device vectors in the context's dot order */
+int rsb_dot(rsb_ctx *ctx, int64_t n, const double *a, const double *b, double *out, int where);
+
+/* ---- preconditioner: RowSplitPreconditioner (pc.py:106-186) ------------- */
+/* perm: row_perm.perm (length m); L1 n x n strict lower (unit diagonal
+ * implied), L2 (m-n) x n, U n x n upper with the diagonal stored last;
+ * Y ((m-n) x n) required for RSB_Y_EXPLICIT; S_factor (s x s lower,
+ * column-major) required for RSB_S_DENSE.  Mirrors build_preconditioner's
+ * checks (pc.py:337-346). */
+int rsb_pre_create(rsb_ctx *ctx, int64_t m, int64_t n, const int64_t *perm, rsb_mat *L1,
+                   rsb_mat *L2, rsb_mat *U, rsb_mat *Y, const double *S_factor, int64_t s,
+                   int s_mode, int y_mode, int cg_iters, rsb_pre **out);
+int rsb_pre_destroy(rsb_pre *pre);
+/* h = apply(r1, r2)             pc.py:167-186 */
+int rsb_pre_apply(rsb_pre *pre, const double *r1, const double *r2, double *h, int where);
+/* Y r1 / Y^T w / S v            pc.py:135-154 */
+int rsb_pre_y_apply(rsb_pre *pre, const double *r1, double *out, int where);
+int rsb_pre_y_apply_transpose(rsb_pre *pre, const double *w, double *out, int where);
+int rsb_pre_s_matvec(rsb_pre *pre, const double *v, double *out, int where);
+
+/* ---- solver: pcgls (sv.py:120-268) -------------------------------------- */
+typedef struct {
+    double norm_A;
+    double delta;
+    int64_t max_iters;
+    int32_t estimator_delay;
+    int32_t ratio_raw;
+} rsb_cgls_cfg; /* CglsConfig sv.py:33-49 */
+
+typedef struct {
+    int64_t its;
+    int64_t iters_run;
+    int32_t converged;
+    int32_t breakdown;
+    double ratio_pt_final;
+    double residual_norm;
+    double gradient_norm;
+    int64_t history_len;
+} rsb_report; /* SolveReport sv.py:52-85 (psize/nmod are host-side) */
+
+/* A solver owns the iteration workspace for one (A, pre) pair and the
+ * captured CUDA graph of one iteration.  pre may be NULL (plain CGLS). */
+int rsb_solver_create(rsb_mat *A, rsb_pre *pre, rsb_solver **out);
+int rsb_solver_destroy(rsb_solver *S);
+/* x = 0, r = b, z = A^T r, h, rho, p (sv.py:147-200).  *status: 0 running,
+ * 4 = z.z == 0 at the start (x = 0 is stationary, sv.py:184-196). */
+int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg,
+                     int *status);
+/* runs up to k iterations (sv.py:202-241); *status: 0 running, 1 converged,
+ * 2 stopped early, 3 iteration cap reached. */
+int rsb_solver_iterate(rsb_solver *S, int64_t k, int64_t *iters_run, int *status);
+int rsb_solver_get_x(rsb_solver *S, double *x, int where);
+/* partial-window certification, final residual and gradient norms
+ * (sv.py:243-266); history gets min(cap, history_len) ratios. */
+int rsb_solver_finish(rsb_solver *S, rsb_report *rep, double *history, int64_t history_cap);
+/* whole solve in one call: start + iterate + finish + get_x */
+int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, double *x,
+              rsb_report *rep, double *history, int64_t history_cap);
+
+/* ---- host setup (stays on the CPU; timed separately) -------------------- */
+/* ilup_factorize (il.py:211-368), bit-identical factors.  Inputs: scaled A
+ * as host CSC.  Query sizes, then copy out. */
+int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *col_ptr, const int64_t *row_idx,
+                       const double *values, int64_t p, double tau, double mu, double small,
+                       rsb_ilup **out);
+int rsb_ilup_sizes(const rsb_ilup *F, int64_t *nnz_l1, int64_t *nnz_l2, int64_t *nnz_u,
+                   int64_t *nmod);
+int rsb_ilup_copy(const rsb_ilup *F, int64_t *perm, int64_t *l1_ptr, int64_t *l1_idx,
+                  double *l1_val, int64_t *l2_ptr, int64_t *l2_idx, double *l2_val,
+                  int64_t *u_ptr, int64_t *u_idx, double *u_val, int64_t *row_counts);
+int rsb_ilup_destroy(rsb_ilup *F);
+/* build_y_explicit (pc.py:55-82): Y = L2 L1^{-1}, host CSC out (two-phase:
+ * call with y_idx == NULL to get *nnz_y, then again with buffers). */
+int rsb_build_y_explicit(int64_t s, int64_t n, const int64_t *l1_ptr, const int64_t *l1_idx,
+                         const double *l1_val, const int64_t *l2_ptr, const int64_t *l2_idx,
+                         const double *l2_val, int64_t *nnz_y, int64_t *y_ptr, int64_t *y_idx,
+                         double *y_val);
+/* dense_cholesky_factorize (sc.py:585-604) in place on an s x s column-major array */
+int rsb_cholesky_factorize(int64_t s, double *g);
+/* column_scale (sc.py:405-425): norms out, scaled values out */
+int rsb_column_scale(int64_t ncols, const int64_t *col_ptr, const double *values,
+                     double *scaled_values, double *norms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROWSPLIT_B200_H */

@@ -1,0 +1,437 @@
+"""CPU oracle for the row-splitting solve phase -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module.  The product package (paper_2603_28642_b200)
+never imports it; its hot path fails loudly without the CUDA library.
+
+This is a restatement of the reference package `rowsplit` (read-only at
+/root/reference/pkg/src/rowsplit; cited as sc.py = sparse_core.py,
+pc.py = precond.py, sv.py = solver.py).  The sparse kernels run in
+oracle/rsref.c in the reference's exact floating-point order (bitwise
+equal, pinned by tests/test_oracle_pin.py against fixtures generated from
+the reference itself); the host loops below follow the reference line by
+line.  Every ``a @ b`` / ``np.linalg.norm`` of the reference goes through
+``dot`` / ``norm`` below, which restate OpenBLAS ddot in the association
+order the reference host uses single-threaded (rsref.c rso_blas_dot), so
+the oracle is bit-identical to the reference with OPENBLAS_NUM_THREADS=1 on
+that host and host-independent everywhere else.
+
+Inputs are duck-typed: any object with nrows/ncols/col_ptr/row_idx/values
+is a CSC matrix, so reference objects and the product package's objects
+both work.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_build", "liboracle_rsref.so")
+_lib = None
+
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            build()
+        L = ctypes.CDLL(_SO)
+        i64, f64 = ctypes.c_int64, ctypes.c_double
+        L.rso_matvec.argtypes = [i64, i64, _i64p, _i64p, _f64p, _f64p, _f64p]
+        L.rso_matvec_transpose.argtypes = [i64, i64, _i64p, _i64p, _f64p, _f64p, _f64p, _f64p]
+        L.rso_lower_solve.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p, ctypes.c_int]
+        L.rso_lower_solve.restype = i64
+        L.rso_upper_solve.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p]
+        L.rso_upper_solve.restype = i64
+        L.rso_lower_solve_transpose.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p, ctypes.c_int]
+        L.rso_lower_solve_transpose.restype = i64
+        L.rso_upper_solve_transpose.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p]
+        L.rso_upper_solve_transpose.restype = i64
+        L.rso_cholesky_factorize.argtypes = [i64, _f64p]
+        L.rso_cholesky_factorize.restype = i64
+        L.rso_cholesky_solve.argtypes = [i64, _f64p, _f64p, _f64p]
+        L.rso_pairwise_sum.argtypes = [_f64p, i64]
+        L.rso_pairwise_sum.restype = f64
+        L.rso_blas_dot.argtypes = [i64, _f64p, _f64p]
+        L.rso_blas_dot.restype = f64
+        _lib = L
+    return _lib
+
+
+def _p64(a):
+    return a.ctypes.data_as(_i64p)
+
+
+def _pf(a):
+    return a.ctypes.data_as(_f64p)
+
+
+def _csc(A):
+    cp = np.ascontiguousarray(A.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(A.row_idx, dtype=np.int64)
+    va = np.ascontiguousarray(A.values, dtype=np.float64)
+    return int(A.nrows), int(A.ncols), cp, ri, va
+
+
+def _vec(v, n):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if v.shape != (n,):
+        raise ValueError(f"vector has shape {v.shape}, expected ({n},)")
+    return v
+
+
+# ---------------------------------------------------------------------------
+# kernels (sc.py)
+# ---------------------------------------------------------------------------
+
+
+def matvec(A, x):
+    """sc.py:212-221."""
+    m, n, cp, ri, va = _csc(A)
+    x = _vec(x, n)
+    y = np.empty(m)
+    lib().rso_matvec(m, n, _p64(cp), _p64(ri), _pf(va), _pf(x), _pf(y))
+    return y
+
+
+def matvec_transpose(A, y):
+    """sc.py:224-235."""
+    m, n, cp, ri, va = _csc(A)
+    y = _vec(y, m)
+    z = np.empty(n)
+    scratch = np.empty(max(1, int(np.diff(cp).max()) if n else 1))
+    lib().rso_matvec_transpose(m, n, _p64(cp), _p64(ri), _pf(va), _pf(y), _pf(z), _pf(scratch))
+    return z
+
+
+def _tri(fn, T, b, *extra):
+    m, n, cp, ri, va = _csc(T)
+    if m != n:
+        raise ValueError("triangular solve needs a square matrix")
+    b = _vec(b, n)
+    x = np.empty(n)
+    rc = fn(n, _p64(cp), _p64(ri), _pf(va), _pf(b), _pf(x), *extra)
+    if rc < 0:
+        raise np.linalg.LinAlgError(f"missing or zero diagonal in column {-rc - 1}")
+    return x
+
+
+def sparse_lower_solve(L, b, unit_diag=False):
+    """sc.py:243-263."""
+    return _tri(lib().rso_lower_solve, L, b, int(bool(unit_diag)))
+
+
+def sparse_upper_solve(U, b):
+    """sc.py:266-279."""
+    return _tri(lib().rso_upper_solve, U, b)
+
+
+def sparse_lower_solve_transpose(L, b, unit_diag=False):
+    """sc.py:282-298."""
+    return _tri(lib().rso_lower_solve_transpose, L, b, int(bool(unit_diag)))
+
+
+def sparse_upper_solve_transpose(U, b):
+    """sc.py:301-313."""
+    return _tri(lib().rso_upper_solve_transpose, U, b)
+
+
+def dense_cholesky_factorize(S):
+    """sc.py:585-604; S is an (s, s) array; returns the lower factor (Fortran order)."""
+    g = np.array(S, dtype=np.float64, order="F", copy=True)
+    s = g.shape[0]
+    rc = lib().rso_cholesky_factorize(s, _pf(g))
+    if rc < 0:
+        raise np.linalg.LinAlgError(f"matrix is not positive definite (pivot {-rc - 1})")
+    return g
+
+
+def dense_cholesky_solve(g, b):
+    """sc.py:607-622; g is the lower factor as an (s, s) array."""
+    g = np.asfortranarray(g, dtype=np.float64)
+    s = g.shape[0]
+    b = _vec(b, s)
+    x = np.empty(s)
+    lib().rso_cholesky_solve(s, _pf(g), _pf(b), _pf(x))
+    return x
+
+
+def dot(a, b):
+    """`a @ b` for 1-D float64 as the reference host's OpenBLAS computes it
+    (single thread; rsref.c rso_blas_dot)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("dot: shape mismatch")
+    return lib().rso_blas_dot(len(a), _pf(a), _pf(b))
+
+
+def norm(a):
+    """np.linalg.norm of a 1-D float64 vector: sqrt(a.dot(a))."""
+    return float(np.sqrt(dot(a, a)))
+
+
+def pairwise_sum(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return lib().rso_pairwise_sum(_pf(a), len(a))
+
+
+def power_method_norm2(A, iters=100, seed=0):
+    """sc.py:428-454."""
+    if iters < 1:
+        raise ValueError("iters must be >= 1")
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(int(A.ncols))
+    nv = norm(v)
+    if nv == 0.0 or int(A.col_ptr[-1]) == 0:
+        return 0.0
+    v /= nv
+    est = 0.0
+    for _ in range(iters):
+        w = matvec(A, v)
+        est = norm(w)
+        if est == 0.0:
+            return 0.0
+        t = matvec_transpose(A, w)
+        nt = norm(t)
+        if nt == 0.0:
+            return est
+        v = t / nt
+    return float(est)
+
+
+# ---------------------------------------------------------------------------
+# preconditioner application (pc.py)
+# ---------------------------------------------------------------------------
+
+
+class OraclePreconditioner:
+    """Applied row-splitting preconditioner, pc.py:106-186.
+
+    factors: object with L1, L2, U (CSC), row_perm.perm, nmod.
+    s_mode: "dense" | "cg" | "identity"; y_mode: "explicit" | "implicit".
+    Y (CSC, explicit mode) and S_factor (s x s lower array, dense mode)
+    come from the caller (built by the reference or by the product setup).
+    """
+
+    def __init__(self, factors, s_mode, y_mode, cg_iters=2, Y=None, S_factor=None, psize=0):
+        self.factors = factors
+        self.s_mode = s_mode
+        self.y_mode = y_mode
+        self.cg_iters = cg_iters
+        self.Y = Y
+        self.S_factor = None if S_factor is None else np.asfortranarray(S_factor)
+        self.psize = psize
+
+    @classmethod
+    def from_reference(cls, pre):
+        """Wrap a reference RowSplitPreconditioner (or a product one)."""
+        S = getattr(pre, "S_factor", None)
+        S = None if S is None else getattr(S, "a", S)
+        sm = getattr(pre.s_mode, "value", pre.s_mode)
+        ym = getattr(pre.y_mode, "value", pre.y_mode)
+        return cls(pre.factors, sm, ym, pre.cg_iters, pre.Y, S, pre.psize)
+
+    @property
+    def n(self):
+        return int(self.factors.U.ncols)
+
+    @property
+    def split_rows(self):
+        return int(self.factors.L2.nrows)
+
+    def y_apply(self, r1):
+        """pc.py:135-139."""
+        if self.y_mode == "explicit":
+            return matvec(self.Y, r1)
+        f = self.factors
+        return matvec(f.L2, sparse_lower_solve(f.L1, r1, unit_diag=True))
+
+    def y_apply_transpose(self, w):
+        """pc.py:141-147."""
+        if self.y_mode == "explicit":
+            return matvec_transpose(self.Y, w)
+        f = self.factors
+        return sparse_lower_solve_transpose(f.L1, matvec_transpose(f.L2, w), unit_diag=True)
+
+    def s_matvec_implicit(self, v):
+        """pc.py:149-154."""
+        f = self.factors
+        v = np.asarray(v, dtype=np.float64)
+        t = matvec_transpose(f.L2, v)
+        t = sparse_lower_solve_transpose(f.L1, t, unit_diag=True)
+        t = sparse_lower_solve(f.L1, t, unit_diag=True)
+        return v + matvec(f.L2, t)
+
+    def _solve_s(self, u):
+        """pc.py:158-163."""
+        if self.s_mode == "dense":
+            return dense_cholesky_solve(self.S_factor, u)
+        if self.s_mode == "identity":
+            return np.array(u, dtype=np.float64, copy=True)
+        return cg_fixed_steps(self.s_matvec_implicit, u, self.cg_iters)
+
+    def apply(self, r1, r2):
+        """pc.py:167-186."""
+        r1 = np.asarray(r1, dtype=np.float64)
+        r2 = np.asarray(r2, dtype=np.float64)
+        if r1.shape != (self.n,) or r2.shape != (self.split_rows,):
+            raise ValueError("residual component lengths do not match the split")
+        if self.split_rows:
+            u = r2 - self.y_apply(r1)
+            w = self._solve_s(u)
+            y = r1 + self.y_apply_transpose(w)
+        else:
+            y = r1
+        v = sparse_lower_solve(self.factors.L1, y, unit_diag=True)
+        return sparse_upper_solve(self.factors.U, v)
+
+
+def cg_fixed_steps(op, u, iters):
+    """pc.py:284-310."""
+    w = np.zeros(len(u))
+    r = np.array(u, dtype=np.float64, copy=True)
+    rho = dot(r, r)
+    if rho == 0.0:
+        return w
+    p = r.copy()
+    for _ in range(iters):
+        q = op(p)
+        pq = dot(p, q)
+        if pq <= 0.0:
+            break
+        alpha = rho / pq
+        w += alpha * p
+        r -= alpha * q
+        rho_new = dot(r, r)
+        if rho_new == 0.0:
+            break
+        p = r + (rho_new / rho) * p
+        rho = rho_new
+    return w
+
+
+# ---------------------------------------------------------------------------
+# solver (sv.py)
+# ---------------------------------------------------------------------------
+
+
+def stopping_ratio(estim, norm_A, x_norm, b_norm, raw=False):
+    """sv.py:104-117."""
+    denom = norm_A * x_norm + b_norm
+    if denom <= 0.0:
+        raise ValueError("zero denominator in stopping ratio")
+    if estim < 0.0:
+        estim = 0.0
+    num = estim if raw else np.sqrt(estim)
+    return float(num / denom)
+
+
+def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
+          iterate_hook=None):
+    """sv.py:120-268.  Returns (x, report dict with SolveReport.to_dict keys)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape != (int(A.nrows),):
+        raise ValueError("right-hand side length mismatch")
+    n = int(A.ncols)
+    b_norm = float(norm(b))
+    if pre is not None:
+        perm = np.asarray(pre.factors.row_perm.perm)
+
+        def precondition(r):
+            rp = r[perm]
+            return pre.apply(rp[:n], rp[n:])
+
+        psize, nmod = pre.psize, pre.factors.nmod
+    else:
+
+        def precondition(r):
+            return matvec_transpose(A, r)
+
+        psize, nmod = 0, 0
+
+    def report(its, converged, breakdown, history, res, grad):
+        return {
+            "its": its, "converged": converged, "breakdown": breakdown,
+            "ratio_pt": history[-1] if history else float("inf"),
+            "ratio_pt_history": list(history), "psize": psize, "nmod": nmod,
+            "residual_norm": res, "gradient_norm": grad,
+        }
+
+    x = np.zeros(n)
+    r = b.copy()
+    z = matvec_transpose(A, r)
+    alphas, sigmas, x_norms, history = [], [], [0.0], []
+    converged = False
+    its_certified = 0
+    iters_run = 0
+    if float(dot(z, z)) == 0.0:
+        return x, report(0, True, False, [0.0], b_norm, 0.0)
+
+    h = precondition(r)
+    rho = float(dot(z, h))
+    p = h.copy()
+    stopped_early = False
+    for it in range(max_iters):
+        sigma = rho if rho > 0.0 else float(dot(z, p))
+        if sigma == 0.0:
+            p = z.copy()
+            sigma = float(dot(z, z))
+            rho = sigma
+        q = matvec(A, p)
+        qq = float(dot(q, q))
+        if qq <= 0.0 or sigma == 0.0:
+            stopped_early = True
+            break
+        alpha = sigma / qq
+        x += alpha * p
+        r -= alpha * q
+        alphas.append(alpha)
+        sigmas.append(sigma)
+        x_norms.append(float(norm(x)))
+        iters_run = it + 1
+        if iterate_hook is not None:
+            iterate_hook(iters_run, x.copy())
+        i = iters_run - d
+        if i >= 0:
+            estim = float(sum(a * s for a, s in zip(alphas[i:], sigmas[i:])))
+            ratio = stopping_ratio(estim, norm_A, x_norms[i], b_norm, raw=ratio_raw)
+            history.append(ratio)
+            if ratio <= delta:
+                converged = True
+                its_certified = i
+                break
+        z = matvec_transpose(A, r)
+        if float(dot(z, z)) == 0.0:
+            stopped_early = True
+            break
+        h = precondition(r)
+        rho_new = float(dot(z, h))
+        p = h + (rho_new / rho) * p if rho != 0.0 else h.copy()
+        rho = rho_new
+
+    if stopped_early and not converged:
+        for i in range(max(0, iters_run - d + 1), iters_run + 1):
+            estim = float(sum(a * s for a, s in zip(alphas[i:], sigmas[i:])))
+            ratio = stopping_ratio(estim, norm_A, x_norms[i], b_norm, raw=ratio_raw)
+            history.append(ratio)
+            if ratio <= delta:
+                converged = True
+                its_certified = i
+                break
+
+    its = its_certified if converged else iters_run
+    fr = b - matvec(A, x)
+    return x, report(its, converged, stopped_early and not converged, history,
+                     float(norm(fr)), float(norm(matvec_transpose(A, fr))))

@@ -1,0 +1,221 @@
+// Level analysis and device layout of the sparse triangular solves
+// (host side, run once per (matrix, kind) and cached on the matrix).
+//
+// The reference solves column by column (sparse_core.py:243-313).  Each
+// unknown's final value is a fixed sequence of operations on other
+// unknowns; this file extracts that sequence per unknown ("task"), in the
+// reference's order, computes the dependency level of every task, sorts the
+// tasks by level and packs their entries in warp-interleaved slices (see
+// TriDev in rsb_internal.h) so the device solve reads them coalesced.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "rsb_internal.h"
+
+namespace rsb {
+
+namespace {
+
+struct Entry {
+    int32_t col;
+    double val;
+};
+
+}  // namespace
+
+int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
+    if (T->nrows != T->ncols) {
+        set_error("triangular solve needs a square matrix");
+        return RSB_EINVAL;
+    }
+    if (T->h_ptr.empty()) {
+        set_error("matrix has no host copy for triangular analysis");
+        return RSB_ESTATE;
+    }
+    const int64_t n = T->ncols;
+    const int64_t *ptr = T->h_ptr.data();
+    const int64_t *idx = T->h_idx.data();
+    const double *val = T->h_val.data();
+
+    const bool unit = (kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T_UNIT);
+    const bool is_dot = (kind == RSB_TRI_LOWER_T || kind == RSB_TRI_LOWER_T_UNIT || kind == RSB_TRI_UPPER_T);
+    const bool lower = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T ||
+                        kind == RSB_TRI_LOWER_T_UNIT);
+    // forward: dependencies of task t are tasks < t
+    const bool forward = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_UPPER_T);
+
+    // diagonal checks in the reference's column visiting order
+    std::vector<double> diag;
+    if (!unit) {
+        diag.assign(n, 0.0);
+        const bool diag_first = lower;
+        const bool asc = (kind == RSB_TRI_LOWER || kind == RSB_TRI_UPPER_T);
+        for (int64_t s = 0; s < n; ++s) {
+            const int64_t j = asc ? s : n - 1 - s;
+            const int64_t lo = ptr[j], hi = ptr[j + 1];
+            const int64_t d = diag_first ? lo : hi - 1;
+            if (hi == lo || idx[d] != j || val[d] == 0.0) {
+                set_error("missing or zero diagonal in column %lld", (long long)j);
+                return RSB_ESINGULAR;
+            }
+            diag[j] = val[d];
+        }
+    }
+    // strict triangularity of the off-diagonal part
+    for (int64_t j = 0; j < n; ++j) {
+        int64_t lo = ptr[j], hi = ptr[j + 1];
+        if (!unit) {
+            if (lower) ++lo; else --hi;
+        }
+        for (int64_t k = lo; k < hi; ++k) {
+            if (lower ? idx[k] <= j : idx[k] >= j) {
+                set_error("matrix is not strictly %s triangular off the diagonal (entry %lld,%lld)",
+                          lower ? "lower" : "upper", (long long)idx[k], (long long)j);
+                return RSB_EINVAL;
+            }
+        }
+    }
+
+    // per-task entry lists in the reference's accumulation order
+    std::vector<int64_t> tptr(n + 1, 0);
+    std::vector<Entry> ent;
+    if (is_dot) {
+        // task j = column j: x_j -= vals @ x[rows] (rows ascending as stored)
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t lo = ptr[j], hi = ptr[j + 1];
+            if (!unit) {
+                if (lower) ++lo; else --hi;
+            }
+            tptr[j + 1] = tptr[j] + (hi - lo);
+        }
+        ent.resize(tptr[n]);
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t lo = ptr[j], hi = ptr[j + 1];
+            if (!unit) {
+                if (lower) ++lo; else --hi;
+            }
+            for (int64_t k = lo; k < hi; ++k) ent[tptr[j] + (k - lo)] = Entry{(int32_t)idx[k], val[k]};
+        }
+    } else {
+        // task i = row i: contributions l_ij x_j in the order columns are visited
+        // (ascending for the lower solve, descending for the upper solve)
+        std::vector<int64_t> cnt(n + 1, 0);
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t lo = ptr[j], hi = ptr[j + 1];
+            if (!unit) {
+                if (lower) ++lo; else --hi;
+            }
+            for (int64_t k = lo; k < hi; ++k) cnt[idx[k] + 1]++;
+        }
+        for (int64_t i = 0; i < n; ++i) tptr[i + 1] = tptr[i] + cnt[i + 1];
+        ent.resize(tptr[n]);
+        std::vector<int64_t> fill(tptr.begin(), tptr.end() - 1);
+        for (int64_t s = 0; s < n; ++s) {
+            const int64_t j = lower ? s : n - 1 - s;
+            int64_t lo = ptr[j], hi = ptr[j + 1];
+            if (!unit) {
+                if (lower) ++lo; else --hi;
+            }
+            for (int64_t k = lo; k < hi; ++k) ent[fill[idx[k]]++] = Entry{(int32_t)j, val[k]};
+        }
+    }
+
+    // dependency levels
+    std::vector<int32_t> level(n, 0);
+    if (forward) {
+        for (int64_t t = 0; t < n; ++t) {
+            int32_t L = 0;
+            for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) L = std::max(L, level[ent[k].col] + 1);
+            level[t] = L;
+        }
+    } else {
+        for (int64_t t = n - 1; t >= 0; --t) {
+            int32_t L = 0;
+            for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) L = std::max(L, level[ent[k].col] + 1);
+            level[t] = L;
+        }
+    }
+    int32_t nlev = 0;
+    for (int64_t t = 0; t < n; ++t) nlev = std::max(nlev, level[t] + 1);
+    std::vector<int64_t> lstart(nlev + 1, 0);
+    for (int64_t t = 0; t < n; ++t) lstart[level[t] + 1]++;
+    int64_t maxw = 0;
+    for (int32_t l = 0; l < nlev; ++l) maxw = std::max(maxw, lstart[l + 1]);
+    for (int32_t l = 0; l < nlev; ++l) lstart[l + 1] += lstart[l];
+    std::vector<int32_t> order(n);
+    {
+        std::vector<int64_t> pos(lstart.begin(), lstart.end() - 1);
+        for (int64_t t = 0; t < n; ++t) order[pos[level[t]]++] = (int32_t)t;
+    }
+
+    // warp-interleaved packing
+    const int64_t nslices = (n + 31) / 32;
+    std::vector<int64_t> soff(nslices + 1, 0);
+    for (int64_t w = 0; w < nslices; ++w) {
+        int64_t K = 0;
+        for (int64_t l = 0; l < 32 && w * 32 + l < n; ++l) {
+            const int32_t t = order[w * 32 + l];
+            K = std::max(K, tptr[t + 1] - tptr[t]);
+        }
+        soff[w + 1] = soff[w] + 32 * K;
+    }
+    const int64_t slots = soff[nslices];
+    std::vector<int32_t> ecol(slots, -1);
+    std::vector<double> eval(slots, 0.0);
+    std::vector<double> tdiag;
+    if (!unit) tdiag.resize(n);
+    for (int64_t w = 0; w < nslices; ++w) {
+        for (int64_t l = 0; l < 32 && w * 32 + l < n; ++l) {
+            const int32_t t = order[w * 32 + l];
+            for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
+                const int64_t e = soff[w] + (k - tptr[t]) * 32 + l;
+                ecol[e] = ent[k].col;
+                eval[e] = ent[k].val;
+            }
+            if (!unit) tdiag[w * 32 + l] = diag[t];
+        }
+    }
+
+    rsb_ctx *ctx = T->ctx;
+    auto *S = new TriSched();
+    S->kind = kind;
+    S->n = (int32_t)n;
+    S->nlevels = nlev;
+    S->max_width = maxw;
+    S->entries = slots;
+    S->mode = (is_dot ? 1 : 0) | (unit ? 0 : 2);
+    int rc = RSB_OK;
+    if ((rc = dev_upload(ctx, &S->task_row, order.data(), n)) != RSB_OK ||
+        (rc = dev_upload(ctx, &S->slice_off, soff.data(), nslices + 1)) != RSB_OK ||
+        (rc = dev_upload(ctx, &S->ecol, ecol.data(), slots)) != RSB_OK ||
+        (rc = dev_upload(ctx, &S->eval, eval.data(), slots)) != RSB_OK ||
+        (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), n)) != RSB_OK) ||
+        (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK) {
+        tri_free(ctx, S);
+        return rc;
+    }
+    cudaError_t e = cudaMemsetAsync(S->ticket, 0, sizeof(unsigned long long), ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // host vectors die here
+    if (e != cudaSuccess) {
+        set_error("CUDA error %s in triangular analysis upload", cudaGetErrorString(e));
+        tri_free(ctx, S);
+        return RSB_ECUDA;
+    }
+    *out = S;
+    return RSB_OK;
+}
+
+void tri_free(rsb_ctx *ctx, TriSched *s) {
+    if (!s) return;
+    const int64_t n = s->n, nslices = (n + 31) / 32;
+    dev_free(ctx, s->task_row, n * sizeof(int32_t));
+    dev_free(ctx, s->slice_off, (nslices + 1) * sizeof(int64_t));
+    dev_free(ctx, s->ecol, s->entries * sizeof(int32_t));
+    dev_free(ctx, s->eval, s->entries * sizeof(double));
+    if (s->diag) dev_free(ctx, s->diag, n * sizeof(double));
+    dev_free(ctx, s->ticket, sizeof(unsigned long long));
+    delete s;
+}
+
+}  // namespace rsb

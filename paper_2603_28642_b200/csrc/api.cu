@@ -1,0 +1,408 @@
+// C ABI: library state, contexts, matrices and the standalone kernels
+// (include/rowsplit_b200.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "rsb_internal.h"
+
+namespace rsb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+int dev_alloc(rsb_ctx *ctx, void **p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 8;  // keep pointers non-null
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        set_error("cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        *p = nullptr;
+        return e == cudaErrorMemoryAllocation ? RSB_ENOMEM : RSB_ECUDA;
+    }
+    ctx->mem_bytes += (int64_t)bytes;
+    return RSB_OK;
+}
+
+void dev_free(rsb_ctx *ctx, void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes == 0) bytes = 8;
+    cudaFree(p);
+    ctx->mem_bytes -= (int64_t)bytes;
+}
+
+Staged::~Staged() {
+    if (owned) dev_free(ctx, d, n * sizeof(double));
+}
+
+int stage_in(rsb_ctx *ctx, const double *p, int64_t n, int where, Staged &s) {
+    s.ctx = ctx;
+    s.n = (size_t)n;
+    if (where == RSB_DEVICE) {
+        s.d = const_cast<double *>(p);
+        return RSB_OK;
+    }
+    RSB_TRY(dev_alloc(ctx, (void **)&s.d, s.n * sizeof(double)));
+    s.owned = true;
+    if (n) RSB_TRY_CUDA(cudaMemcpyAsync(s.d, p, s.n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    return RSB_OK;
+}
+
+int stage_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s) {
+    s.ctx = ctx;
+    s.n = (size_t)n;
+    if (where == RSB_DEVICE) {
+        s.d = p;
+        return RSB_OK;
+    }
+    RSB_TRY(dev_alloc(ctx, (void **)&s.d, s.n * sizeof(double)));
+    s.owned = true;
+    return RSB_OK;
+}
+
+int finish_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s) {
+    if (where == RSB_HOST && n)
+        RSB_TRY_CUDA(cudaMemcpyAsync(p, s.d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RSB_OK;
+}
+
+int get_tri(rsb_mat *T, int kind, TriSched **out) {
+    if (kind < 0 || kind > 5) {
+        set_error("unknown triangular solve kind %d", kind);
+        return RSB_EINVAL;
+    }
+    if (!T->tri[kind]) RSB_TRY(tri_analyse(T, kind, &T->tri[kind]));
+    *out = T->tri[kind];
+    return RSB_OK;
+}
+
+}  // namespace rsb
+
+using namespace rsb;
+
+extern "C" {
+
+const char *rsb_last_error(void) { return g_last_error.c_str(); }
+
+int rsb_version(void) { return 100; }
+
+int rsb_device_count(int *count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *count = c;
+    return RSB_OK;
+}
+
+int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
+    *out = nullptr;
+    int count = 0;
+    rsb_device_count(&count);
+    if (count == 0) {
+        set_error("no CUDA device available: the B200 solve path has no CPU fallback");
+        return RSB_ECUDA;
+    }
+    if (device < 0 || device >= count) {
+        set_error("device %d out of range (%d devices)", device, count);
+        return RSB_EINVAL;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RSB_TRY_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        set_error("device %d is sm_%d%d; this library is built for sm_100a (B200)", device, prop.major,
+                  prop.minor);
+        return RSB_ECUDA;
+    }
+    auto *ctx = new rsb_ctx();
+    ctx->device = device;
+    ctx->flags = flags;
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < 16; ++i) e = cudaEventCreate(&ctx->ev[i]);
+    if (e == cudaSuccess) e = cudaMallocHost((void **)&ctx->h_scalar, 64 * sizeof(double));
+    if (e != cudaSuccess) {
+        set_error("context setup failed: %s", cudaGetErrorString(e));
+        delete ctx;
+        return RSB_ECUDA;
+    }
+    int rc = dev_alloc(ctx, (void **)&ctx->d_scalar, 64 * sizeof(double));
+    if (rc == RSB_OK) {
+        ctx->partial_cap = 2 * 148 * 4;
+        rc = dev_alloc(ctx, (void **)&ctx->d_partials, ctx->partial_cap * sizeof(double));
+    }
+    if (rc != RSB_OK) {
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return RSB_OK;
+}
+
+int rsb_ctx_destroy(rsb_ctx *ctx) {
+    if (!ctx) return RSB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    dev_free(ctx, ctx->d_scalar, 64 * sizeof(double));
+    dev_free(ctx, ctx->d_partials, ctx->partial_cap * sizeof(double));
+    if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return RSB_OK;
+}
+
+int rsb_ctx_sync(rsb_ctx *ctx) {
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RSB_OK;
+}
+
+int rsb_ctx_kernel_launches(rsb_ctx *ctx, int64_t *count, int reset) {
+    *count = ctx->launches;
+    if (reset) ctx->launches = 0;
+    return RSB_OK;
+}
+
+int rsb_ctx_mem_bytes(rsb_ctx *ctx, int64_t *bytes) {
+    *bytes = ctx->mem_bytes;
+    return RSB_OK;
+}
+
+int rsb_host_alloc(int64_t bytes, void **ptr) {
+    RSB_TRY_CUDA(cudaMallocHost(ptr, (size_t)std::max<int64_t>(bytes, 8)));
+    return RSB_OK;
+}
+
+int rsb_host_free(void *ptr) {
+    RSB_TRY_CUDA(cudaFreeHost(ptr));
+    return RSB_OK;
+}
+
+int rsb_device_alloc(rsb_ctx *ctx, int64_t bytes, void **ptr) { return dev_alloc(ctx, ptr, (size_t)bytes); }
+
+int rsb_device_free(rsb_ctx *ctx, void *ptr) {
+    // size unknown here: untracked frees only adjust the CUDA allocator
+    RSB_TRY_CUDA(cudaFree(ptr));
+    return RSB_OK;
+}
+
+int rsb_memcpy(rsb_ctx *ctx, void *dst, const void *src, int64_t bytes, int kind) {
+    cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    RSB_TRY_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, ctx->stream));
+    return RSB_OK;
+}
+
+int rsb_event_mark(rsb_ctx *ctx, int slot) {
+    if (slot < 0 || slot >= 16) {
+        set_error("event slot %d out of range", slot);
+        return RSB_EINVAL;
+    }
+    RSB_TRY_CUDA(cudaEventRecord(ctx->ev[slot], ctx->stream));
+    return RSB_OK;
+}
+
+int rsb_event_elapsed(rsb_ctx *ctx, int slot0, int slot1, float *ms) {
+    RSB_TRY_CUDA(cudaEventSynchronize(ctx->ev[slot1]));
+    RSB_TRY_CUDA(cudaEventElapsedTime(ms, ctx->ev[slot0], ctx->ev[slot1]));
+    return RSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// matrices
+// ---------------------------------------------------------------------------
+
+int rsb_mat_create(rsb_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *col_ptr,
+                   const int64_t *row_idx, const double *values, rsb_mat **out) {
+    *out = nullptr;
+    if (nrows < 0 || ncols < 0 || nrows >= INT32_MAX || ncols >= INT32_MAX) {
+        set_error("matrix dimensions %lld x %lld out of range", (long long)nrows, (long long)ncols);
+        return RSB_EINVAL;
+    }
+    const int64_t nnz = col_ptr[ncols];
+    if (col_ptr[0] != 0 || nnz < 0 || nnz >= INT32_MAX) {
+        set_error("col_ptr endpoints invalid or nnz %lld beyond the int32 device index range", (long long)nnz);
+        return RSB_EINVAL;
+    }
+    for (int64_t j = 0; j < ncols; ++j)
+        if (col_ptr[j + 1] < col_ptr[j]) {
+            set_error("col_ptr not non-decreasing");
+            return RSB_EINVAL;
+        }
+    for (int64_t k = 0; k < nnz; ++k)
+        if (row_idx[k] < 0 || row_idx[k] >= nrows) {
+            set_error("row index out of range");
+            return RSB_EINVAL;
+        }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    auto *A = new rsb_mat();
+    A->ctx = ctx;
+    A->nrows = nrows;
+    A->ncols = ncols;
+    A->nnz = nnz;
+    A->h_ptr.assign(col_ptr, col_ptr + ncols + 1);
+    A->h_idx.assign(row_idx, row_idx + nnz);
+    A->h_val.assign(values, values + nnz);
+    // CSC, int32
+    std::vector<int32_t> cp(ncols + 1), ci(nnz);
+    for (int64_t j = 0; j <= ncols; ++j) cp[j] = (int32_t)col_ptr[j];
+    int32_t maxc = 0;
+    for (int64_t j = 0; j < ncols; ++j) maxc = std::max<int32_t>(maxc, cp[j + 1] - cp[j]);
+    for (int64_t k = 0; k < nnz; ++k) ci[k] = (int32_t)row_idx[k];
+    // CSR: rows filled by visiting columns in ascending order (the scatter
+    // order of np.add.at in sc.py:220)
+    std::vector<int32_t> rp(nrows + 1, 0), ri(nnz);
+    std::vector<double> rv(nnz);
+    for (int64_t k = 0; k < nnz; ++k) rp[row_idx[k] + 1]++;
+    for (int64_t i = 0; i < nrows; ++i) rp[i + 1] += rp[i];
+    int32_t maxr = 0;
+    for (int64_t i = 0; i < nrows; ++i) maxr = std::max<int32_t>(maxr, rp[i + 1] - rp[i]);
+    {
+        std::vector<int32_t> fill(rp.begin(), rp.end() - 1);
+        for (int64_t j = 0; j < ncols; ++j)
+            for (int64_t k = col_ptr[j]; k < col_ptr[j + 1]; ++k) {
+                const int32_t d = fill[row_idx[k]]++;
+                ri[d] = (int32_t)j;
+                rv[d] = values[k];
+            }
+    }
+    A->max_row_len = maxr;
+    A->max_col_len = maxc;
+    int rc = RSB_OK;
+    if ((rc = dev_upload(ctx, &A->c_ptr, cp.data(), cp.size())) != RSB_OK ||
+        (rc = dev_upload(ctx, &A->c_idx, ci.data(), ci.size())) != RSB_OK ||
+        (rc = dev_upload(ctx, &A->c_val, values, (size_t)nnz)) != RSB_OK ||
+        (rc = dev_upload(ctx, &A->r_ptr, rp.data(), rp.size())) != RSB_OK ||
+        (rc = dev_upload(ctx, &A->r_idx, ri.data(), ri.size())) != RSB_OK ||
+        (rc = dev_upload(ctx, &A->r_val, rv.data(), rv.size())) != RSB_OK) {
+        rsb_mat_destroy(A);
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        set_error("matrix upload failed: %s", cudaGetErrorString(e));
+        rsb_mat_destroy(A);
+        return RSB_ECUDA;
+    }
+    *out = A;
+    return RSB_OK;
+}
+
+int rsb_mat_destroy(rsb_mat *A) {
+    if (!A) return RSB_OK;
+    rsb_ctx *ctx = A->ctx;
+    cudaStreamSynchronize(ctx->stream);
+    dev_free(ctx, A->c_ptr, (A->ncols + 1) * sizeof(int32_t));
+    dev_free(ctx, A->c_idx, A->nnz * sizeof(int32_t));
+    dev_free(ctx, A->c_val, A->nnz * sizeof(double));
+    dev_free(ctx, A->r_ptr, (A->nrows + 1) * sizeof(int32_t));
+    dev_free(ctx, A->r_idx, A->nnz * sizeof(int32_t));
+    dev_free(ctx, A->r_val, A->nnz * sizeof(double));
+    for (auto &t : A->tri) tri_free(ctx, t);
+    delete A;
+    return RSB_OK;
+}
+
+int rsb_mat_info(const rsb_mat *A, int64_t *nrows, int64_t *ncols, int64_t *nnz) {
+    *nrows = A->nrows;
+    *ncols = A->ncols;
+    *nnz = A->nnz;
+    return RSB_OK;
+}
+
+int rsb_matvec(rsb_mat *A, const double *x, double *y, int where) {
+    rsb_ctx *ctx = A->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged sx, sy;
+    RSB_TRY(stage_in(ctx, x, A->ncols, where, sx));
+    RSB_TRY(stage_out(ctx, y, A->nrows, where, sy));
+    RSB_TRY(launch_spmv(ctx, A->csr(), VecIn{sx.d, nullptr, 0}, sy.d, EPI_STORE, VecIn{}, Gate{}));
+    return finish_out(ctx, y, A->nrows, where, sy);
+}
+
+int rsb_matvec_transpose(rsb_mat *A, const double *y, double *z, int where) {
+    rsb_ctx *ctx = A->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged sy, sz;
+    RSB_TRY(stage_in(ctx, y, A->nrows, where, sy));
+    RSB_TRY(stage_out(ctx, z, A->ncols, where, sz));
+    RSB_TRY(launch_spmv_t(ctx, A->csc(), VecIn{sy.d, nullptr, 0}, sz.d, EPI_STORE, VecIn{}, Gate{}));
+    return finish_out(ctx, z, A->ncols, where, sz);
+}
+
+int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where) {
+    rsb_ctx *ctx = T->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    TriSched *S = nullptr;
+    RSB_TRY(get_tri(T, kind, &S));
+    Staged sb, sx;
+    RSB_TRY(stage_in(ctx, b, T->ncols, where, sb));
+    RSB_TRY(stage_out(ctx, x, T->ncols, where, sx));
+    if (sb.d == sx.d && T->ncols) {
+        set_error("rsb_trsv: b and x must not alias");
+        return RSB_EINVAL;
+    }
+    RSB_TRY(launch_trsv(ctx, *S, VecIn{sb.d, nullptr, 0}, nullptr, sx.d, Gate{}));
+    return finish_out(ctx, x, T->ncols, where, sx);
+}
+
+int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width) {
+    TriSched *S = nullptr;
+    RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
+    RSB_TRY(get_tri(T, kind, &S));
+    *nlevels = S->nlevels;
+    *max_width = S->max_width;
+    return RSB_OK;
+}
+
+int rsb_chol_solve(rsb_ctx *ctx, int64_t s, const double *G, const double *b, double *x, int where) {
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    if (s < 0) {
+        set_error("negative size");
+        return RSB_EINVAL;
+    }
+    Staged sg, sb, sx;
+    sg.ctx = ctx;
+    if (where == RSB_DEVICE) {
+        sg.d = const_cast<double *>(G);
+    } else {
+        RSB_TRY(dev_alloc(ctx, (void **)&sg.d, (size_t)(s * s) * sizeof(double)));
+        sg.owned = true;
+        sg.n = (size_t)(s * s);
+        if (s) RSB_TRY_CUDA(cudaMemcpyAsync(sg.d, G, (size_t)(s * s) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    RSB_TRY(stage_in(ctx, b, s, where, sb));
+    RSB_TRY(stage_out(ctx, x, s, where, sx));
+    RSB_TRY(prepare_chol(s));
+    RSB_TRY(launch_chol_solve(ctx, sg.d, s, sb.d, sx.d, Gate{}));
+    return finish_out(ctx, x, s, where, sx);
+}
+
+int rsb_dot(rsb_ctx *ctx, int64_t n, const double *a, const double *b, double *out, int where) {
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged sa, sb;
+    RSB_TRY(stage_in(ctx, a, n, where, sa));
+    RSB_TRY(stage_in(ctx, b, n, where, sb));
+    RSB_TRY(launch_dot(ctx, n, VecIn{sa.d, nullptr, 0}, VecIn{sb.d, nullptr, 0}, ctx->d_scalar, 0, Gate{},
+                       nullptr));
+    RSB_TRY_CUDA(cudaMemcpyAsync(ctx->h_scalar, ctx->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->h_scalar[0];
+    return RSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,601 @@
+// Host setup kept on the CPU (north star: "the serial ILUP threshold-pivoting
+// factorization stays in the host setup, is timed separately, and produces
+// factors the GPU path consumes unchanged").
+//
+// Native restatements, bit-identical to the reference package, of
+//   ilup_factorize     pkg/src/rowsplit/ilup.py:211-368 (il.py)
+//   build_y_explicit   pkg/src/rowsplit/precond.py:55-82 (with the
+//                      sparse-RHS solve of sparse_core.py:328-397)
+//   dense_cholesky_factorize  sparse_core.py:585-604
+//   column_scale       sparse_core.py:405-425
+// so the B200 path can be set up at the BASELINE sizes on a box that has no
+// copy of the reference (the reference's Python ILUP needs ~1.5 h for config
+// 4 at mu = 1 and months at mu = 0.1).  Every operation keeps
+// the reference's order and rounding: numpy elementwise ops are one IEEE
+// operation each, compiled here with -ffp-contract=off.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "../../include/rowsplit_b200.h"
+
+namespace rsb {
+void set_error(const char *fmt, ...);
+}
+using rsb::set_error;
+
+struct rsb_ilup {
+    int64_t m = 0, n = 0, nmod = 0;
+    std::vector<int64_t> row_at, pos_of, rc;
+    std::vector<int64_t> l1_ptr, l1_idx, l2_ptr, l2_idx, u_ptr, u_idx;
+    std::vector<double> l1_val, l2_val, u_val;
+};
+
+namespace {
+
+// numpy pairwise summation (same recipe as the device kernels)
+double pairwise(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (int64_t i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int k = 0; k < 8; ++k) r[k] = a[k];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise(a, n2) + pairwise(a + n2, n - n2);
+}
+
+// _dual_drop (il.py:159-167): keep |v| >= tau and v != 0; if more than p
+// remain keep the p largest |v| (ties: smaller id first); return sorted by id.
+void dual_drop(std::vector<int64_t> &ids, std::vector<double> &vals, int64_t p, double tau) {
+    size_t k = 0;
+    for (size_t i = 0; i < ids.size(); ++i)
+        if (std::fabs(vals[i]) >= tau && vals[i] != 0.0) {
+            ids[k] = ids[i];
+            vals[k] = vals[i];
+            ++k;
+        }
+    ids.resize(k);
+    vals.resize(k);
+    std::vector<size_t> ord(k);
+    std::iota(ord.begin(), ord.end(), 0);
+    if ((int64_t)k > p) {
+        // np.lexsort((ids, -abs(vals))): primary -|v| ascending, secondary id
+        std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+            const double na = -std::fabs(vals[a]), nb = -std::fabs(vals[b]);
+            if (na != nb) return na < nb;
+            return ids[a] < ids[b];
+        });
+        ord.resize(p);
+    }
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+    std::vector<int64_t> ni(ord.size());
+    std::vector<double> nv(ord.size());
+    for (size_t i = 0; i < ord.size(); ++i) {
+        ni[i] = ids[ord[i]];
+        nv[i] = vals[ord[i]];
+    }
+    ids.swap(ni);
+    vals.swap(nv);
+}
+
+// CscMatrix.from_coo for entries without duplicates or zeros (the factor
+// assembly of il.py:349-359): sort rows inside every column.
+void coo_to_csc(int64_t ncols, const std::vector<int64_t> &rows, const std::vector<int64_t> &cols,
+                const std::vector<double> &vals, std::vector<int64_t> &ptr, std::vector<int64_t> &idx,
+                std::vector<double> &val) {
+    const size_t nnz = rows.size();
+    ptr.assign(ncols + 1, 0);
+    for (size_t k = 0; k < nnz; ++k) ptr[cols[k] + 1]++;
+    for (int64_t j = 0; j < ncols; ++j) ptr[j + 1] += ptr[j];
+    idx.resize(nnz);
+    val.resize(nnz);
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t k = 0; k < nnz; ++k) {
+        const int64_t d = fill[cols[k]]++;
+        idx[d] = rows[k];
+        val[d] = vals[k];
+    }
+    std::vector<std::pair<int64_t, double>> tmp;
+    for (int64_t j = 0; j < ncols; ++j) {
+        const int64_t lo = ptr[j], hi = ptr[j + 1];
+        bool sorted = true;
+        for (int64_t k = lo + 1; k < hi; ++k)
+            if (idx[k] < idx[k - 1]) {
+                sorted = false;
+                break;
+            }
+        if (sorted) continue;
+        tmp.clear();
+        for (int64_t k = lo; k < hi; ++k) tmp.emplace_back(idx[k], val[k]);
+        std::sort(tmp.begin(), tmp.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
+        for (int64_t k = lo; k < hi; ++k) {
+            idx[k] = tmp[k - lo].first;
+            val[k] = tmp[k - lo].second;
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *ptr, const int64_t *ridx, const double *avals,
+                       int64_t p, double tau, double mu, double small, rsb_ilup **out) {
+    *out = nullptr;
+    if (p < 1 || tau < 0.0 || !(mu > 0.0 && mu <= 1.0) || !(small > 0.0)) {
+        set_error("invalid IlupParams");
+        return RSB_EINVAL;
+    }
+    if (n < 1 || m < 1) {
+        set_error("empty matrix");
+        return RSB_EINVAL;
+    }
+    if (m < n) {
+        set_error("need nrows >= ncols, got %lld x %lld", (long long)m, (long long)n);
+        return RSB_EINVAL;
+    }
+    auto F = new rsb_ilup();
+    F->m = m;
+    F->n = n;
+    std::vector<int64_t> &row_at = F->row_at, &pos_of = F->pos_of, &rc = F->rc;
+    row_at.resize(m);
+    pos_of.resize(m);
+    std::iota(row_at.begin(), row_at.end(), 0);
+    std::iota(pos_of.begin(), pos_of.end(), 0);
+    rc.assign(m, 0);  // remaining_row_counts (il.py:153-156)
+    for (int64_t k = 0; k < ptr[n]; ++k) rc[ridx[k]]++;
+    std::vector<double> col_inf(n, 0.0);  // np.maximum.reduceat(|A|) (il.py:235-238)
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) col_inf[j] = std::max(col_inf[j], std::fabs(avals[k]));
+
+    // l_rows[q]: original row ids of L column q (order as kept), u per column
+    std::vector<int64_t> l_ptr(1, 0), l_rows;
+    std::vector<double> l_vals;
+    std::vector<std::vector<int64_t>> u_rows(n);
+    std::vector<std::vector<double>> u_vals(n);
+
+    std::vector<double> x(m, 0.0);
+    std::vector<char> mark(m, 0);
+    std::vector<int64_t> pattern, u_pos, cand, kept;
+    std::vector<double> u_val, cval, kept_v;
+    std::vector<int64_t> post, stack_node, stack_cur;
+    int64_t nmod = 0;
+
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t alo = ptr[j], ahi = ptr[j + 1], alen = ahi - alo;
+        for (int64_t k = alo; k < ahi; ++k) x[ridx[k]] = avals[k];
+        pattern.assign(ridx + alo, ridx + ahi);
+        u_pos.clear();
+        u_val.clear();
+        if (j == 0 || alen == 0) {
+            for (int64_t k = alo; k < ahi; ++k) mark[ridx[k]] = 1;
+        } else if (alen >= std::max<int64_t>(8, j / 8)) {
+            // dense-ish column: sweep pivot positions in order (il.py:258-279)
+            for (int64_t k = alo; k < ahi; ++k) mark[ridx[k]] = 1;
+            for (int64_t q = 0; q < j; ++q) {
+                const int64_t u = row_at[q];
+                const double xu = x[u];
+                if (xu == 0.0) continue;
+                u_pos.push_back(q);
+                u_val.push_back(xu);
+                for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
+                    const int64_t r = l_rows[e];
+                    const double c = l_vals[e] * xu;
+                    x[r] = x[r] - c;
+                }
+                for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
+                    const int64_t r = l_rows[e];
+                    if (!mark[r]) {
+                        mark[r] = 1;
+                        pattern.push_back(r);
+                    }
+                }
+            }
+        } else {
+            // sparse column: DFS reach over the partial factor (il.py:170-208)
+            pattern.clear();
+            post.clear();
+            for (int64_t k = alo; k < ahi; ++k) {
+                const int64_t s = ridx[k];
+                if (mark[s]) continue;
+                mark[s] = 1;
+                pattern.push_back(s);
+                if (pos_of[s] >= j) continue;
+                stack_node.assign(1, s);
+                stack_cur.assign(1, 0);
+                while (!stack_node.empty()) {
+                    const int64_t node = stack_node.back();
+                    int64_t cursor = stack_cur.back();
+                    const int64_t q = pos_of[node];
+                    const int64_t clo = l_ptr[q], clen = l_ptr[q + 1] - clo;
+                    bool advanced = false;
+                    while (cursor < clen) {
+                        const int64_t child = l_rows[clo + cursor];
+                        ++cursor;
+                        if (!mark[child]) {
+                            mark[child] = 1;
+                            pattern.push_back(child);
+                            if (pos_of[child] < j) {
+                                stack_cur.back() = cursor;
+                                stack_node.push_back(child);
+                                stack_cur.push_back(0);
+                                advanced = true;
+                                break;
+                            }
+                        }
+                    }
+                    if (!advanced) {
+                        stack_node.pop_back();
+                        stack_cur.pop_back();
+                        post.push_back(node);
+                    }
+                }
+            }
+            // eliminate reached pivots in topological order (reversed post-order)
+            for (auto it = post.rbegin(); it != post.rend(); ++it) {
+                const int64_t u = *it;
+                const double xu = x[u];
+                if (xu == 0.0) continue;
+                const int64_t q = pos_of[u];
+                u_pos.push_back(q);
+                u_val.push_back(xu);
+                for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
+                    const int64_t r = l_rows[e];
+                    const double c = l_vals[e] * xu;
+                    x[r] = x[r] - c;
+                }
+            }
+        }
+
+        dual_drop(u_pos, u_val, p, tau);  // il.py:300
+
+        // active part: reached rows not yet pivotal, nonzero (il.py:303-307)
+        cand.clear();
+        cval.clear();
+        for (int64_t r : pattern)
+            if (pos_of[r] >= j && x[r] != 0.0) {
+                cand.push_back(r);
+                cval.push_back(x[r]);
+            }
+
+        int64_t pivot_orig;
+        double pivot_val;
+        // modify_pivot (il.py:142-150)
+        auto modified = [&]() {
+            const double beta = std::pow(10.0, -2.0 * (1.0 - (double)(j + 1) / (double)n));
+            return std::max(beta * col_inf[j], small);
+        };
+        if (cand.empty()) {
+            pivot_orig = row_at[j];
+            pivot_val = modified();
+            ++nmod;
+        } else {
+            // choose_pivot (il.py:122-139): |v| >= mu * max|v|, then fewest
+            // remaining row entries, then smallest position
+            double mx = std::fabs(cval[0]);
+            bool has_nan = std::isnan(mx);
+            for (size_t i = 1; i < cval.size(); ++i) {
+                const double a = std::fabs(cval[i]);
+                if (std::isnan(a)) has_nan = true;
+                mx = std::max(mx, a);
+            }
+            if (has_nan) {
+                set_error("non-finite value in column %lld of the factorization", (long long)j);
+                delete F;
+                return RSB_ESINGULAR;
+            }
+            const double thr = mu * mx;
+            int64_t best = -1;
+            for (size_t i = 0; i < cand.size(); ++i) {
+                if (!(std::fabs(cval[i]) >= thr)) continue;
+                if (best < 0) {
+                    best = (int64_t)i;
+                    continue;
+                }
+                const int64_t rb = rc[cand[best]], ri = rc[cand[i]];
+                if (ri < rb || (ri == rb && pos_of[cand[i]] < pos_of[cand[best]])) best = (int64_t)i;
+            }
+            pivot_orig = row_at[pos_of[cand[best]]];
+            pivot_val = x[pivot_orig];
+            if (std::fabs(pivot_val) < small) {
+                pivot_val = modified();
+                ++nmod;
+            }
+            size_t k = 0;
+            for (size_t i = 0; i < cand.size(); ++i)
+                if (cand[i] != pivot_orig) {
+                    cand[k] = cand[i];
+                    cval[k] = cval[i];
+                    ++k;
+                }
+            cand.resize(k);
+            cval.resize(k);
+        }
+
+        // interchange (il.py:324-328)
+        const int64_t q = pos_of[pivot_orig];
+        if (q != j) {
+            const int64_t other = row_at[j];
+            row_at[j] = pivot_orig;
+            row_at[q] = other;
+            pos_of[pivot_orig] = j;
+            pos_of[other] = q;
+        }
+
+        // scale, then drop in the L column by current position (il.py:331-339)
+        kept.clear();
+        kept_v.clear();
+        for (size_t i = 0; i < cand.size(); ++i) {
+            kept.push_back(pos_of[cand[i]]);
+            kept_v.push_back(cval[i] / pivot_val);
+        }
+        dual_drop(kept, kept_v, p, tau);
+        for (size_t i = 0; i < kept.size(); ++i) {
+            l_rows.push_back(row_at[kept[i]]);
+            l_vals.push_back(kept_v[i]);
+        }
+        l_ptr.push_back((int64_t)l_rows.size());
+
+        u_rows[j] = u_pos;
+        u_rows[j].push_back(j);
+        u_vals[j] = u_val;
+        u_vals[j].push_back(pivot_val);
+
+        for (int64_t k = alo; k < ahi; ++k) rc[ridx[k]] -= 1;
+        for (int64_t r : pattern) {
+            x[r] = 0.0;
+            mark[r] = 0;
+        }
+    }
+    F->nmod = nmod;
+
+    // assemble in final pivot coordinates (il.py:349-359)
+    {
+        std::vector<int64_t> rr, cc;
+        std::vector<double> vv;
+        for (int64_t j = 0; j < n; ++j)
+            for (size_t k = 0; k < u_rows[j].size(); ++k) {
+                rr.push_back(u_rows[j][k]);
+                cc.push_back(j);
+                vv.push_back(u_vals[j][k]);
+            }
+        coo_to_csc(n, rr, cc, vv, F->u_ptr, F->u_idx, F->u_val);
+    }
+    {
+        std::vector<int64_t> r1, c1, r2, c2;
+        std::vector<double> v1, v2;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t e = l_ptr[j]; e < l_ptr[j + 1]; ++e) {
+                const int64_t pos = pos_of[l_rows[e]];
+                if (pos < n) {
+                    r1.push_back(pos);
+                    c1.push_back(j);
+                    v1.push_back(l_vals[e]);
+                } else {
+                    r2.push_back(pos - n);
+                    c2.push_back(j);
+                    v2.push_back(l_vals[e]);
+                }
+            }
+        coo_to_csc(n, r1, c1, v1, F->l1_ptr, F->l1_idx, F->l1_val);
+        coo_to_csc(n, r2, c2, v2, F->l2_ptr, F->l2_idx, F->l2_val);
+    }
+    *out = F;
+    return RSB_OK;
+}
+
+int rsb_ilup_sizes(const rsb_ilup *F, int64_t *nnz_l1, int64_t *nnz_l2, int64_t *nnz_u, int64_t *nmod) {
+    *nnz_l1 = (int64_t)F->l1_idx.size();
+    *nnz_l2 = (int64_t)F->l2_idx.size();
+    *nnz_u = (int64_t)F->u_idx.size();
+    *nmod = F->nmod;
+    return RSB_OK;
+}
+
+int rsb_ilup_copy(const rsb_ilup *F, int64_t *perm, int64_t *l1_ptr, int64_t *l1_idx, double *l1_val,
+                  int64_t *l2_ptr, int64_t *l2_idx, double *l2_val, int64_t *u_ptr, int64_t *u_idx,
+                  double *u_val, int64_t *row_counts) {
+    auto cp = [](auto *dst, const auto &src) {
+        if (dst && !src.empty()) std::memcpy(dst, src.data(), src.size() * sizeof(src[0]));
+    };
+    cp(perm, F->row_at);
+    cp(l1_ptr, F->l1_ptr);
+    cp(l1_idx, F->l1_idx);
+    cp(l1_val, F->l1_val);
+    cp(l2_ptr, F->l2_ptr);
+    cp(l2_idx, F->l2_idx);
+    cp(l2_val, F->l2_val);
+    cp(u_ptr, F->u_ptr);
+    cp(u_idx, F->u_idx);
+    cp(u_val, F->u_val);
+    cp(row_counts, F->rc);
+    return RSB_OK;
+}
+
+int rsb_ilup_destroy(rsb_ilup *F) {
+    delete F;
+    return RSB_OK;
+}
+
+// build_y_explicit (pc.py:55-82): row i of Y solves L1^T y = (row i of L2)
+// by a sparse-RHS solve (sc.py:365-397) whose DFS order (sc.py:328-362)
+// fixes the floating-point order; exact zeros from cancellation are dropped
+// (pc.py:70-71).
+int rsb_build_y_explicit(int64_t s, int64_t n, const int64_t *l1_ptr, const int64_t *l1_idx,
+                         const double *l1_val, const int64_t *l2_ptr, const int64_t *l2_idx,
+                         const double *l2_val, int64_t *nnz_y, int64_t *y_ptr, int64_t *y_idx, double *y_val) {
+    // T = L1^T and L2^T as CSC (CscMatrix.transpose -> from_coo: rows sorted)
+    std::vector<int64_t> tp(n + 1, 0), ti;
+    std::vector<double> tv;
+    {
+        const int64_t nnz = l1_ptr[n];
+        for (int64_t k = 0; k < nnz; ++k) tp[l1_idx[k] + 1]++;
+        for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+        ti.resize(nnz);
+        tv.resize(nnz);
+        std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t k = l1_ptr[j]; k < l1_ptr[j + 1]; ++k) {
+                const int64_t d = fill[l1_idx[k]]++;
+                ti[d] = j;
+                tv[d] = l1_val[k];
+            }
+    }
+    std::vector<int64_t> bp(s + 1, 0), bi;
+    std::vector<double> bv;
+    {
+        const int64_t nnz = l2_ptr[n];
+        for (int64_t k = 0; k < nnz; ++k) bp[l2_idx[k] + 1]++;
+        for (int64_t i = 0; i < s; ++i) bp[i + 1] += bp[i];
+        bi.resize(nnz);
+        bv.resize(nnz);
+        std::vector<int64_t> fill(bp.begin(), bp.end() - 1);
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t k = l2_ptr[j]; k < l2_ptr[j + 1]; ++k) {
+                const int64_t d = fill[l2_idx[k]]++;
+                bi[d] = j;
+                bv[d] = l2_val[k];
+            }
+    }
+    std::vector<int64_t> yr, yc;
+    std::vector<double> yv;
+    std::vector<double> x(n, 0.0);
+    std::vector<char> marked(n, 0);
+    std::vector<int64_t> topo, sn, sc;
+    for (int64_t i = 0; i < s; ++i) {
+        const int64_t lo = bp[i], hi = bp[i + 1];
+        if (hi == lo) continue;
+        // reach_pattern (sc.py:328-362): iterative DFS, reversed post-order
+        topo.clear();
+        for (int64_t k = lo; k < hi; ++k) {
+            const int64_t sd = bi[k];
+            if (marked[sd]) continue;
+            marked[sd] = 1;
+            sn.assign(1, sd);
+            sc.assign(1, tp[sd]);
+            while (!sn.empty()) {
+                const int64_t node = sn.back();
+                int64_t cursor = sc.back();
+                bool adv = false;
+                while (cursor < tp[node + 1]) {
+                    const int64_t child = ti[cursor];
+                    ++cursor;
+                    if (child != node && !marked[child]) {
+                        marked[child] = 1;
+                        sc.back() = cursor;
+                        sn.push_back(child);
+                        sc.push_back(tp[child]);
+                        adv = true;
+                        break;
+                    }
+                }
+                if (!adv) {
+                    sn.pop_back();
+                    sc.pop_back();
+                    topo.push_back(node);
+                }
+            }
+        }
+        std::reverse(topo.begin(), topo.end());
+        for (int64_t k = lo; k < hi; ++k) x[bi[k]] = bv[k];
+        for (int64_t node : topo) {  // unit diagonal: no division
+            const double xv = x[node];
+            if (xv != 0.0)
+                for (int64_t t = tp[node]; t < tp[node + 1]; ++t) {
+                    const int64_t r = ti[t];
+                    if (r != node) {
+                        const double c = tv[t] * xv;
+                        x[r] = x[r] - c;
+                    }
+                }
+        }
+        std::vector<int64_t> pat(topo);
+        std::sort(pat.begin(), pat.end());
+        for (int64_t c : pat) {
+            if (x[c] != 0.0) {
+                yr.push_back(i);
+                yc.push_back(c);
+                yv.push_back(x[c]);
+            }
+            x[c] = 0.0;
+            marked[c] = 0;
+        }
+    }
+    const int64_t nnz = (int64_t)yr.size();
+    if (!y_idx) {
+        *nnz_y = nnz;
+        return RSB_OK;
+    }
+    if (*nnz_y < nnz) {
+        set_error("Y buffer too small");
+        return RSB_EINVAL;
+    }
+    std::vector<int64_t> p, idx;
+    std::vector<double> val;
+    coo_to_csc(n, yr, yc, yv, p, idx, val);
+    std::memcpy(y_ptr, p.data(), (n + 1) * sizeof(int64_t));
+    if (nnz) {
+        std::memcpy(y_idx, idx.data(), nnz * sizeof(int64_t));
+        std::memcpy(y_val, val.data(), nnz * sizeof(double));
+    }
+    *nnz_y = nnz;
+    return RSB_OK;
+}
+
+// dense_cholesky_factorize (sc.py:585-604), lower factor in place
+int rsb_cholesky_factorize(int64_t s, double *g) {
+    for (int64_t j = 0; j < s; ++j) {
+        double d = g[j + j * s];
+        if (d <= 0.0 || !std::isfinite(d)) {
+            set_error("matrix is not positive definite (pivot %lld)", (long long)j);
+            return RSB_ESINGULAR;
+        }
+        d = std::sqrt(d);
+        g[j + j * s] = d;
+        for (int64_t i = j + 1; i < s; ++i) g[i + j * s] /= d;
+        for (int64_t k = j + 1; k < s; ++k) {
+            const double gk = g[k + j * s];
+            for (int64_t i = j + 1; i < s; ++i) {
+                const double c = g[i + j * s] * gk;
+                g[i + k * s] = g[i + k * s] - c;
+            }
+        }
+    }
+    for (int64_t k = 1; k < s; ++k)
+        for (int64_t i = 0; i < k; ++i) g[i + k * s] = 0.0;
+    return RSB_OK;
+}
+
+// column_scale (sc.py:405-425): sq_j = reduceat(v*v) = p0 + pairwise(rest)
+int rsb_column_scale(int64_t ncols, const int64_t *ptr, const double *values, double *scaled, double *norms) {
+    std::vector<double> sq;
+    for (int64_t j = 0; j < ncols; ++j) {
+        const int64_t lo = ptr[j], hi = ptr[j + 1];
+        if (hi == lo) {
+            set_error("cannot scale zero column %lld", (long long)j);
+            return RSB_EINVAL;
+        }
+        sq.resize(hi - lo);
+        for (int64_t k = lo; k < hi; ++k) sq[k - lo] = values[k] * values[k];
+        const double s2 = sq[0] + pairwise(sq.data() + 1, hi - lo - 1);
+        norms[j] = std::sqrt(s2);
+    }
+    for (int64_t j = 0; j < ncols; ++j)
+        for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) scaled[k] = values[k] / norms[j];
+    return RSB_OK;
+}
+
+}  // extern "C"

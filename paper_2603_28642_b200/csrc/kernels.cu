@@ -1,0 +1,488 @@
+// Hot-path kernels of the B200 solve phase (sm_100a, FP64 CUDA cores).
+//
+// Every kernel reproduces the floating-point operation order of the
+// reference's numpy/OpenBLAS code (pkg/src/rowsplit/sparse_core.py = sc.py),
+// so results are bit-identical to it.  The file is compiled with
+// -fmad=false: a*b+c is two roundings unless fma() is written out.
+#include <cuda_runtime.h>
+
+#include "rsb_internal.h"
+
+namespace rsb {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kTriBlock = 128;
+
+__device__ __forceinline__ bool gated(const Gate &g) {
+    return (g.a && *(volatile const int *)g.a) || (g.b && *(volatile const int *)g.b);
+}
+
+__device__ __forceinline__ double vin(const VecIn &v, int64_t i) {
+    return v.g ? v.p[v.g[i + v.off]] : v.p[i + v.off];
+}
+
+// ---------------------------------------------------------------------------
+// OpenBLAS ddot association (SkylakeX kernel, one thread), one warp:
+//   n1 = n & -16 through the vector kernel -- four 8-wide FMA accumulators
+//   over 32-blocks (lane l holds accumulator l), folded 8 -> 4 (lo+hi half),
+//   a trailing 16-block into four 4-wide accumulators, lane-wise
+//   ((a0+a1)+a2)+a3, then (t0+t2)+(t1+t3); the tail is a scalar FMA chain.
+// Bit-identical to numpy `a @ b` on the reference host (oracle/rsref.c
+// rso_blas_dot, tests/test_oracle_pin.py).  All lanes must call; the
+// result is valid in every lane.
+// ---------------------------------------------------------------------------
+template <class LA, class LB>
+__device__ __forceinline__ double warp_blas_dot(int64_t n, LA la, LB lb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n1 = n & ~(int64_t)15;
+    const int64_t n32 = n1 & ~(int64_t)31;
+    double acc = 0.0;
+    int64_t i = lane;
+    // unrolled FMA chain: loads of 8 blocks issued ahead of the dependent FMAs
+    for (; i + 7 * 32 < n32; i += 8 * 32) {
+        double xa[8], xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xa[u] = la(i + u * 32);
+            xb[u] = lb(i + u * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(xa[u], xb[u], acc);
+    }
+    for (; i < n32; i += 32) acc = fma(la(i), lb(i), acc);
+    // fold a5[g][k] + a5[g][k+4] into lane 8g+k (k < 4)
+    double hi = __shfl_down_sync(0xffffffffu, acc, 4);
+    double a4 = acc + hi;  // meaningful in lanes with (lane & 7) < 4
+    if (n1 > n32) {
+        const int g = lane >> 3, k = lane & 7;
+        if (k < 4) {
+            const int64_t e = n32 + 4 * g + k;
+            a4 = fma(la(e), lb(e), a4);
+        }
+    }
+    // t[k] = ((a[0][k] + a[1][k]) + a[2][k]) + a[3][k], a[g][k] in lane 8g+k
+    double a1 = __shfl_down_sync(0xffffffffu, a4, 8);
+    double a2 = __shfl_down_sync(0xffffffffu, a4, 16);
+    double a3 = __shfl_down_sync(0xffffffffu, a4, 24);
+    double t = ((a4 + a1) + a2) + a3;  // valid in lanes 0..3
+    double t1 = __shfl_sync(0xffffffffu, t, 1);
+    double t2 = __shfl_sync(0xffffffffu, t, 2);
+    double t3 = __shfl_sync(0xffffffffu, t, 3);
+    double t0 = __shfl_sync(0xffffffffu, t, 0);
+    double dot = n1 ? (t0 + t2) + (t1 + t3) : 0.0;
+    for (int64_t e = n1; e < n; ++e) dot = fma(lb(e), la(e), dot);
+    return dot;
+}
+
+__global__ void k_dot_exact(int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
+                            const int *need) {
+    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    double d = warp_blas_dot(
+        n, [&](int64_t i) { return vin(a, i); }, [&](int64_t i) { return vin(b, i); });
+    if (threadIdx.x == 0) out[0] = sqrt_out ? sqrt(d) : d;
+}
+
+// Fixed-shape two-level tree (RSB_DOT_TREE): block b sums a fixed chunk in a
+// fixed order; the finisher sums the partials in index order.  Deterministic
+// for a given n, not the reference's association.
+__global__ void k_dot_tree_partial(int64_t n, VecIn a, VecIn b, double *partials, Gate g,
+                                   const int *need) {
+    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    __shared__ double sh[kBlock];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * chunk;
+    const int64_t hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kBlock) acc = fma(vin(a, i), vin(b, i), acc);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = kBlock / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+__global__ void k_dot_tree_final(int nparts, const double *partials, double *out, int sqrt_out,
+                                 Gate g, const int *need) {
+    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    if (threadIdx.x == 0) {
+        double d = 0.0;
+        for (int i = 0; i < nparts; ++i) d = d + partials[i];
+        out[0] = sqrt_out ? sqrt(d) : d;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// y = A x: numpy's np.add.at scatter (sc.py:218-220) accumulates row i's
+// contributions in ascending column order starting from 0.0, one rounding
+// for the product and one for the add -- i.e. a CSR row-sequential sum.
+// ---------------------------------------------------------------------------
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) k_spmv(Compressed A, VecIn x, double *y, VecIn e, Gate g) {
+    if (gated(g)) return;
+    const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    if (i >= A.nlines) return;
+    const int lo = A.ptr[i], hi = A.ptr[i + 1];
+    double acc = 0.0;
+    for (int k = lo; k < hi; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], vin(x, A.idx[k])));
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, i), acc);
+    if (EPI == EPI_SUB_FROM) acc = __dsub_rn(vin(e, i), acc);
+    y[i] = acc;
+}
+
+// numpy pairwise summation (DOUBLE_pairwise_sum) of products val[k]*y[idx[k]],
+// k = lo .. lo+n-1
+__device__ double pw_prod(const double *val, const int32_t *idx, const VecIn &y, int64_t lo,
+                          int64_t n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, __dmul_rn(val[lo + i], vin(y, idx[lo + i])));
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = __dmul_rn(val[lo + k], vin(y, idx[lo + k]));
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                r[k] = __dadd_rn(r[k], __dmul_rn(val[lo + i + k], vin(y, idx[lo + i + k])));
+        }
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn(val[lo + i], vin(y, idx[lo + i])));
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    double left = pw_prod(val, idx, y, lo, n2);
+    double right = pw_prod(val, idx, y, lo + n2, n - n2);
+    return __dadd_rn(left, right);
+}
+
+// z = A^T y: np.add.reduceat over the column's products (sc.py:231-234)
+// gives z_j = p0 + pairwise(p1 .. p_{k-1}); empty columns stay 0.0.
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) k_spmv_t(Compressed At, VecIn y, double *z, VecIn e, Gate g) {
+    if (gated(g)) return;
+    const int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    if (j >= At.nlines) return;
+    const int lo = At.ptr[j], hi = At.ptr[j + 1];
+    double acc = 0.0;
+    if (hi > lo) {
+        double p0 = __dmul_rn(At.val[lo], vin(y, At.idx[lo]));
+        acc = __dadd_rn(p0, pw_prod(At.val, At.idx, y, lo + 1, hi - lo - 1));
+    }
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, j), acc);
+    z[j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// Sync-free level-ordered triangular solve.
+//
+// One thread per unknown.  Tasks are sorted by dependency level and blocks
+// take consecutive task ranges in the order they start (atomic ticket), so a
+// task only ever waits on tasks of blocks that are already running or done.
+// The output vector itself is the completion flag: it is pre-filled with a
+// sentinel NaN and a task spins (L2-coherent relaxed loads) until each of
+// its inputs is no longer the sentinel.  Sequential mode reproduces the
+// reference's column-oriented axpy (sc.py:253-262, 271-278):
+//   x_i = b_i; for each dependency j in stored order: if x_j != 0: x_i -= l_ij*x_j
+// then x_i /= d_i when a diagonal is stored.  Dot mode reproduces
+// x_j -= vals @ x[rows] (sc.py:291,296,311): an OpenBLAS ddot of the gathered
+// values (FMA chain below 16 entries, SkylakeX blocking above).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double wait_ready(const double *p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == kSentinel);
+    return __longlong_as_double(v);
+}
+
+__device__ __forceinline__ void publish(double *p, double v) {
+    unsigned long long b = __double_as_longlong(v);
+    if (b == kSentinel) b = 0x7FF8000000000000ull;
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
+}
+
+// blas-order dot of a task's gathered entries, one thread (len >= 16 path)
+__device__ double task_blas_dot(const TriDev &T, int64_t base, int lane, int len, const double *x) {
+    auto ent = [&](int k) { return base + (int64_t)k * 32 + lane; };
+    const int n1 = len & ~15, n32 = n1 & ~31;
+    double dot = 0.0;
+    if (n1) {
+        double a5[32];
+        for (int q = 0; q < 32; ++q) a5[q] = 0.0;
+        int i = 0;
+        for (; i < n32; i += 32)
+            for (int q = 0; q < 32; ++q)
+                a5[q] = fma(T.eval[ent(i + q)], wait_ready(x + T.ecol[ent(i + q)]), a5[q]);
+        double a[16];
+        for (int gq = 0; gq < 4; ++gq)
+            for (int k = 0; k < 4; ++k) a[4 * gq + k] = a5[8 * gq + k] + a5[8 * gq + k + 4];
+        for (; i < n1; i += 16)
+            for (int q = 0; q < 16; ++q)
+                a[q] = fma(T.eval[ent(i + q)], wait_ready(x + T.ecol[ent(i + q)]), a[q]);
+        double t[4];
+        for (int k = 0; k < 4; ++k) t[k] = ((a[k] + a[4 + k]) + a[8 + k]) + a[12 + k];
+        dot = (t[0] + t[2]) + (t[1] + t[3]);
+    }
+    for (int k = n1; k < len; ++k) dot = fma(wait_ready(x + T.ecol[ent(k)]), T.eval[ent(k)], dot);
+    return dot;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const double *c, double *x,
+                                                    Gate g) {
+    if (gated(g)) return;
+    __shared__ int s_blk;
+    if (threadIdx.x == 0) s_blk = (int)(atomicAdd(T.ticket, 1ull) % gridDim.x);
+    __syncthreads();
+    const int t = s_blk * kTriBlock + threadIdx.x;
+    if (t >= T.n) return;
+    const int row = T.task_row[t];
+    double acc = vin(a, row);
+    if (c) acc = __dadd_rn(acc, c[row]);
+    const int w = t >> 5, lane = t & 31;
+    const int64_t base = T.slice_off[w];
+    const int K = (int)((T.slice_off[w + 1] - base) >> 5);
+    if (!(MODE & 1)) {
+        for (int k = 0; k < K; ++k) {
+            const int j = T.ecol[base + (int64_t)k * 32 + lane];
+            if (j < 0) break;
+            const double v = T.eval[base + (int64_t)k * 32 + lane];
+            const double xj = wait_ready(x + j);
+            if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(v, xj));
+        }
+    } else {
+        int len = 0;
+        while (len < K && T.ecol[base + (int64_t)len * 32 + lane] >= 0) ++len;
+        if (len > 0) {
+            double dot;
+            if (len < 16) {
+                dot = 0.0;
+                for (int k = 0; k < len; ++k) {
+                    const int64_t e = base + (int64_t)k * 32 + lane;
+                    dot = fma(T.eval[e], wait_ready(x + T.ecol[e]), dot);
+                }
+            } else {
+                dot = task_blas_dot(T, base, lane, len, x);
+            }
+            acc = __dsub_rn(acc, dot);
+        }
+    }
+    if (MODE & 2) acc = __ddiv_rn(acc, T.diag[t]);
+    publish(x + row, acc);
+}
+
+// ---------------------------------------------------------------------------
+// small vector kernels
+// ---------------------------------------------------------------------------
+__global__ void k_fill(double *x, int64_t n, unsigned long long bits, Gate g) {
+    if (gated(g)) return;
+    const double v = __longlong_as_double(bits);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_copy(double *dst, VecIn src, int64_t n, Gate g) {
+    if (gated(g)) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = vin(src, i);
+}
+
+// y += s*x  /  y -= s*x   (x += alpha*p, r -= alpha*q: sv.py:215-216, pc.py:303-304)
+template <int SIGN>
+__global__ void k_axpy(double *y, const double *x, const double *scal, int64_t n, Gate g) {
+    if (gated(g)) return;
+    const double s = *scal;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = __dmul_rn(s, x[i]);
+        y[i] = SIGN > 0 ? __dadd_rn(y[i], t) : __dsub_rn(y[i], t);
+    }
+}
+
+// p = h + beta*p (sv.py:240, pc.py:308) or p = h.copy() when copy_flag set
+__global__ void k_xpby(double *p, const double *h, const double *beta, const int *copy_flag,
+                       int64_t n, Gate g) {
+    if (gated(g)) return;
+    const bool cp = copy_flag && *copy_flag;
+    const double b = cp ? 0.0 : *beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = cp ? h[i] : __dadd_rn(h[i], __dmul_rn(b, p[i]));
+}
+
+// ---------------------------------------------------------------------------
+// Dense Cholesky solve S w = u with the lower column-major factor G
+// (sc.py:607-622), one CTA.  Forward: column axpy x[j+1:] -= g[j+1:,j]*x[j]
+// (parallel over rows, sequential over j -- the reference's order for every
+// element).  Backward: x[j] -= g[j+1:,j] @ x[j+1:] as a warp-level OpenBLAS
+// ddot (same association as the host), then x[j] /= g[j,j].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_chol_solve(const double *G, int64_t s, const double *u,
+                                                      double *w, int use_smem, Gate g) {
+    if (gated(g)) return;
+    extern __shared__ double sx[];
+    double *x = use_smem ? sx : w;
+    for (int64_t i = threadIdx.x; i < s; i += kBlock) x[i] = u[i];
+    __syncthreads();
+    for (int64_t j = 0; j < s; ++j) {
+        const double xj = __ddiv_rn(x[j], G[j + j * s]);
+        __syncthreads();
+        if (threadIdx.x == 0) x[j] = xj;
+        for (int64_t i = j + 1 + threadIdx.x; i < s; i += kBlock)
+            x[i] = __dsub_rn(x[i], __dmul_rn(G[i + j * s], xj));
+        __syncthreads();
+    }
+    if (threadIdx.x < 32) {
+        for (int64_t j = s - 1; j >= 0; --j) {
+            double xj = x[j];
+            if (j + 1 < s) {
+                const double *gc = G + (j + 1) + j * s;
+                const double *xc = x + j + 1;
+                const double d = warp_blas_dot(
+                    s - j - 1, [&](int64_t i) { return gc[i]; }, [&](int64_t i) { return xc[i]; });
+                xj = __dsub_rn(xj, d);
+            }
+            xj = __ddiv_rn(xj, G[j + j * s]);
+            __syncwarp();
+            if (threadIdx.x == 0) x[j] = xj;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (use_smem)
+        for (int64_t i = threadIdx.x; i < s; i += kBlock) w[i] = x[i];
+}
+
+inline int grid_for(int64_t n, int block) {
+    int64_t b = (n + block - 1) / block;
+    return (int)(b < 1 ? 1 : (b > (1 << 30) ? (1 << 30) : b));
+}
+
+inline int grid_stride(int64_t n) {
+    // elementwise kernels: up to 8 waves of 148 SMs x 8 resident blocks
+    int64_t b = (n + kBlock - 1) / kBlock;
+    int64_t cap = 148 * 8 * 8;
+    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+inline int post_launch(rsb_ctx *ctx, int kernels = 1) {
+    ctx->launches += kernels;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("kernel launch failed: %s", cudaGetErrorString(e));
+        return RSB_ECUDA;
+    }
+    return RSB_OK;
+}
+
+}  // namespace
+
+int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
+    if (A.nlines == 0) return RSB_OK;
+    const int grid = grid_for(A.nlines, kBlock);
+    switch (epi) {
+        case EPI_STORE: k_spmv<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+        case EPI_ADD: k_spmv<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+        default: k_spmv<EPI_SUB_FROM><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+    }
+    return post_launch(ctx);
+}
+
+int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
+    if (At.nlines == 0) return RSB_OK;
+    const int grid = grid_for(At.nlines, kBlock);
+    if (epi == EPI_ADD)
+        k_spmv_t<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+    else
+        k_spmv_t<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+    return post_launch(ctx);
+}
+
+int launch_fill(rsb_ctx *ctx, double *x, int64_t n, unsigned long long bits, Gate g) {
+    if (n == 0) return RSB_OK;
+    k_fill<<<grid_stride(n), kBlock, 0, ctx->stream>>>(x, n, bits, g);
+    return post_launch(ctx);
+}
+
+int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g) {
+    if (T.n == 0) return RSB_OK;
+    RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
+    const int grid = grid_for(T.n, kTriBlock);
+    const TriDev v = T.view();
+    switch (T.mode) {
+        case 0: k_trsv<0><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+        case 1: k_trsv<1><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+        case 2: k_trsv<2><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+        default: k_trsv<3><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+    }
+    return post_launch(ctx);
+}
+
+int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
+               const int *need) {
+    if ((ctx->flags & RSB_DOT_TREE) && n > 4096) {
+        int parts = (int)std::min<int64_t>((n + 8191) / 8192, 2 * 148 * 4);
+        if (parts > ctx->partial_cap) {
+            set_error("tree-dot partial buffer too small");
+            return RSB_ESTATE;
+        }
+        k_dot_tree_partial<<<parts, kBlock, 0, ctx->stream>>>(n, a, b, ctx->d_partials, g, need);
+        RSB_TRY(post_launch(ctx));
+        k_dot_tree_final<<<1, 32, 0, ctx->stream>>>(parts, ctx->d_partials, out, sqrt_out, g, need);
+        return post_launch(ctx);
+    }
+    k_dot_exact<<<1, 32, 0, ctx->stream>>>(n, a, b, out, sqrt_out, g, need);
+    return post_launch(ctx);
+}
+
+int launch_copy(rsb_ctx *ctx, double *dst, VecIn src, int64_t n, Gate g) {
+    if (n == 0) return RSB_OK;
+    k_copy<<<grid_stride(n), kBlock, 0, ctx->stream>>>(dst, src, n, g);
+    return post_launch(ctx);
+}
+
+int launch_axpy(rsb_ctx *ctx, double *y, const double *x, const double *scal, int sign, int64_t n,
+                Gate g) {
+    if (n == 0) return RSB_OK;
+    if (sign > 0)
+        k_axpy<1><<<grid_stride(n), kBlock, 0, ctx->stream>>>(y, x, scal, n, g);
+    else
+        k_axpy<-1><<<grid_stride(n), kBlock, 0, ctx->stream>>>(y, x, scal, n, g);
+    return post_launch(ctx);
+}
+
+int launch_xpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, const int *copy_flag,
+                int64_t n, Gate g) {
+    if (n == 0) return RSB_OK;
+    k_xpby<<<grid_stride(n), kBlock, 0, ctx->stream>>>(p, h, beta, copy_flag, n, g);
+    return post_launch(ctx);
+}
+
+int prepare_chol(int64_t s) {
+    const size_t smem = (size_t)s * sizeof(double);
+    if (smem > 48 * 1024 && smem <= 200 * 1024)
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    return RSB_OK;
+}
+
+int launch_chol_solve(rsb_ctx *ctx, const double *G, int64_t s, const double *u, double *w, Gate g) {
+    if (s == 0) return RSB_OK;
+    const size_t smem = (size_t)s * sizeof(double);
+    const int use_smem = smem <= 200 * 1024;
+    k_chol_solve<<<1, kBlock, use_smem ? smem : 0, ctx->stream>>>(G, s, u, w, use_smem, g);
+    return post_launch(ctx);
+}
+
+}  // namespace rsb

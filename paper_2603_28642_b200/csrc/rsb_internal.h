@@ -1,0 +1,213 @@
+// Internal declarations of librowsplit_b200.so (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/rowsplit_b200.h"
+
+namespace rsb {
+
+void set_error(const char *fmt, ...);
+
+#define RSB_TRY_CUDA(call)                                                                  \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) {                                                            \
+            rsb::set_error("CUDA error %s in %s (%s:%d)", cudaGetErrorString(e_), #call,    \
+                           __FILE__, __LINE__);                                             \
+            return RSB_ECUDA;                                                               \
+        }                                                                                   \
+    } while (0)
+
+#define RSB_TRY(call)                \
+    do {                             \
+        int rc_ = (call);            \
+        if (rc_ != RSB_OK) return rc_; \
+    } while (0)
+
+// Sentinel marking "not yet solved" entries of a triangular-solve output.  A
+// signalling-NaN payload: FP64 arithmetic only ever produces quiet NaNs, and
+// the solve kernel rewrites a copied input that happens to carry these exact
+// bits, so no finished entry can look unfinished.
+constexpr unsigned long long kSentinel = 0xFFF4D15EA5E0C0DEull;
+
+// ---------------------------------------------------------------------------
+// device-side views (passed by value to kernels)
+// ---------------------------------------------------------------------------
+
+// Compressed sparse rows (or columns, for the transposed product): entries of
+// line i are idx/val[ptr[i] .. ptr[i+1]) in the order the reference adds them.
+struct Compressed {
+    int32_t nlines;  // rows for CSR, columns for CSC
+    int32_t nother;
+    int64_t nnz;
+    const int32_t *ptr;
+    const int32_t *idx;
+    const double *val;
+};
+
+// A vector operand, optionally read through a gather: v(i) = p[g[i + off]]
+// (g == nullptr: p[i + off]).  Used to fuse the residual's pivot-order split
+// r[perm] (sv.py:159-161) into the consumers.
+struct VecIn {
+    const double *p;
+    const int32_t *g;
+    int64_t off;
+};
+
+// Skip predicate for kernels of a device-side control loop: a kernel does no
+// work when *a != 0 or (b && *b != 0).  Used to reproduce the reference's
+// `break`s (sv.py:211-213,229-237; pc.py:294-307) without host syncs.
+struct Gate {
+    const int *a;
+    const int *b;
+};
+
+// Level-ordered triangular-solve schedule: task t solves unknown task_row[t];
+// tasks are sorted by dependency level, so every dependency of task t is a task
+// < t.  Warp slice w (tasks 32w..32w+31) stores its entries interleaved --
+// entry k of lane l at slice_off[w] + 32k + l -- in the reference's
+// accumulation order; padding has col == -1.
+struct TriDev {
+    int32_t n;
+    int32_t mode;  // bit0: dot (FMA/BLAS order) instead of sequential axpy; bit1: divide by diag
+    const int32_t *task_row;
+    const int64_t *slice_off;
+    const int32_t *ecol;
+    const double *eval;
+    const double *diag;  // per task, nullptr when unit
+    unsigned long long *ticket;
+};
+
+// ---------------------------------------------------------------------------
+// host-side objects behind the opaque handles
+// ---------------------------------------------------------------------------
+
+struct Ctx;
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct TriSched {
+    int kind = -1;
+    int32_t n = 0;
+    int64_t nlevels = 0;
+    int64_t max_width = 0;
+    int64_t entries = 0;  // padded entry slots
+    int32_t *task_row = nullptr;
+    int64_t *slice_off = nullptr;
+    int32_t *ecol = nullptr;
+    double *eval = nullptr;
+    double *diag = nullptr;
+    unsigned long long *ticket = nullptr;
+    int32_t mode = 0;
+    TriDev view() const {
+        return TriDev{n, mode, task_row, slice_off, ecol, eval, diag, ticket};
+    }
+};
+
+}  // namespace rsb
+
+struct rsb_ctx {
+    int device = 0;
+    int flags = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int64_t mem_bytes = 0;
+    cudaEvent_t ev[16] = {};
+    // small device scratch for standalone dots / scalars
+    double *d_scalar = nullptr;
+    double *h_scalar = nullptr;  // pinned
+    // tree-dot partials
+    double *d_partials = nullptr;
+    int partial_cap = 0;
+};
+
+struct rsb_mat {
+    rsb_ctx *ctx = nullptr;
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    // CSR of A (row sequential order, sc.py:220) and CSC of A (sc.py:231-234)
+    int32_t *r_ptr = nullptr, *r_idx = nullptr;
+    double *r_val = nullptr;
+    int32_t *c_ptr = nullptr, *c_idx = nullptr;
+    double *c_val = nullptr;
+    int32_t max_row_len = 0, max_col_len = 0;
+    // host CSC kept for lazily analysed triangular schedules
+    std::vector<int64_t> h_ptr, h_idx;
+    std::vector<double> h_val;
+    rsb::TriSched *tri[6] = {};
+    rsb::Compressed csr() const {
+        return rsb::Compressed{(int32_t)nrows, (int32_t)ncols, nnz, r_ptr, r_idx, r_val};
+    }
+    rsb::Compressed csc() const {
+        return rsb::Compressed{(int32_t)ncols, (int32_t)nrows, nnz, c_ptr, c_idx, c_val};
+    }
+};
+
+namespace rsb {
+
+// memory helpers (tracked per context)
+int dev_alloc(rsb_ctx *ctx, void **p, size_t bytes);
+void dev_free(rsb_ctx *ctx, void *p, size_t bytes);
+template <class T>
+int dev_upload(rsb_ctx *ctx, T **dst, const T *src, size_t count) {
+    RSB_TRY(dev_alloc(ctx, (void **)dst, count * sizeof(T)));
+    if (count) RSB_TRY_CUDA(cudaMemcpyAsync(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return RSB_OK;
+}
+
+// Host-or-device vector staging for the standalone entry points (api.cu).
+struct Staged {
+    rsb_ctx *ctx = nullptr;
+    double *d = nullptr;
+    size_t n = 0;
+    bool owned = false;
+    ~Staged();
+};
+int stage_in(rsb_ctx *ctx, const double *p, int64_t n, int where, Staged &s);
+int stage_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s);
+int finish_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s);
+// cached level-ordered schedule of (matrix, kind)
+int get_tri(rsb_mat *T, int kind, TriSched **out);
+// one-time kernel attribute setup for the dense S solve of size s
+int prepare_chol(int64_t s);
+
+// triangular-solve analysis (analysis.cpp)
+int tri_analyse(rsb_mat *T, int kind, TriSched **out);
+void tri_free(rsb_ctx *ctx, TriSched *s);
+
+// ---------------------------------------------------------------------------
+// kernel launchers (kernels.cu); all enqueue on ctx->stream
+// ---------------------------------------------------------------------------
+enum EpiOp { EPI_STORE = 0, EPI_ADD = 1, EPI_SUB_FROM = 2 };
+// y(i) = acc (STORE) | e(i) + acc (ADD) | e(i) - acc (SUB_FROM),
+// acc = sequential row sum of A x from 0.0 (sc.py:218-220)
+int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g);
+// z(j) = acc | e(j) + acc, acc = p0 + pairwise(p1..), p = vals * y[rows] (sc.py:231-234)
+int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g);
+// triangular solve of a schedule: x(row) = solve with rhs(row) = a(row) [+ c[row]]
+int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g);
+// out[0] = a.b (sqrt_out: sqrt(a.b)) in the context's dot order; need: optional
+// flag that must be nonzero for the dot to run
+int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
+               const int *need);
+int launch_fill(rsb_ctx *ctx, double *x, int64_t n, unsigned long long bits, Gate g);
+int launch_copy(rsb_ctx *ctx, double *dst, VecIn src, int64_t n, Gate g);
+// y = y + s*x (sign=+1) or y = y - s*x (sign=-1), s = *scal
+int launch_axpy(rsb_ctx *ctx, double *y, const double *x, const double *scal, int sign, int64_t n,
+                Gate g);
+// p = h + (*beta) * p, or p = h when *copy_flag != 0
+int launch_xpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, const int *copy_flag,
+                int64_t n, Gate g);
+// dense Cholesky solve with the lower column-major factor (sc.py:607-622)
+int launch_chol_solve(rsb_ctx *ctx, const double *G, int64_t s, const double *u, double *w, Gate g);
+
+}  // namespace rsb

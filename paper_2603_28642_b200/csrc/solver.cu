@@ -1,0 +1,896 @@
+// Preconditioner application, device-resident pcgls and the power method.
+//
+// The host never looks at a scalar inside an iteration: dots land in a
+// device-side state block, one-thread "control" kernels evaluate the
+// reference's branches there, and every vector kernel carries a Gate that
+// turns it into a no-op once the control state says the reference would
+// have left the loop.  One pcgls iteration is captured once as a CUDA graph
+// and replayed; the host only polls the 4-byte status between batches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "rsb_internal.h"
+
+namespace rsb {
+
+// ---------------------------------------------------------------------------
+// device control state
+// ---------------------------------------------------------------------------
+struct CgState {  // _cg_fixed_steps, pc.py:284-310
+    double rho, pq, alpha, rho_new, beta;
+    int stop;
+};
+
+enum Status { ST_RUN = 0, ST_CONVERGED = 1, ST_STOPPED = 2, ST_MAXED = 3, ST_ZERO_START = 4, ST_ERROR = 5 };
+
+struct CglsState {  // pcgls locals, sv.py:147-241
+    double norm_A, delta, b_norm;
+    double rho, sigma, alpha, qq, zz, zh, zp, beta, xnorm;
+    long long max_iters, iters_run, its_certified, hist_len;
+    int d, ratio_raw;
+    int status;
+    int need_zp, skip_retry, p_copy;
+};
+
+struct PowerState {  // power_method_norm2, sc.py:428-454
+    double nv, est, nt, result;
+    int stop;
+};
+
+namespace {
+
+// Python 3.12 sum() of floats (Neumaier compensated), as used by
+// error_estimate (sv.py:101) and the partial-window sums (sv.py:247):
+// sum(a*s for ...) with an int 0 start.
+__host__ __device__ inline double py_sum_products(const double *a, const double *s, long long lo,
+                                                  long long hi) {
+    if (hi <= lo) return 0.0;
+    double f = 0.0 + a[lo] * s[lo];
+    double c = 0.0;
+    for (long long k = lo + 1; k < hi; ++k) {
+        const double x = a[k] * s[k];
+        const double t = f + x;
+        if (fabs(f) >= fabs(x))
+            c += (f - t) + x;
+        else
+            c += (x - t) + f;
+        f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f += c;
+    return f;
+}
+
+// stopping_ratio, sv.py:104-117 (error flag on a non-positive denominator)
+__host__ __device__ inline double py_stopping_ratio(double estim, double norm_A, double x_norm,
+                                                    double b_norm, int raw, int *err) {
+    const double denom = norm_A * x_norm + b_norm;
+    if (denom <= 0.0) {
+        *err = 1;
+        return 0.0;
+    }
+    if (estim < 0.0) estim = 0.0;
+    const double num = raw ? estim : sqrt(estim);
+    return num / denom;
+}
+
+__device__ __forceinline__ bool gated(const Gate &g) {
+    return (g.a && *(volatile const int *)g.a) || (g.b && *(volatile const int *)g.b);
+}
+
+// ---- inner CG control (pc.py:291-309) ----
+__global__ void k_cg_start(CgState *cg, Gate g) {  // rho = r@r; if rho == 0: return w (=0)
+    if (gated(g)) return;
+    cg->stop = (cg->rho == 0.0) ? 1 : 0;
+}
+__global__ void k_cg_alpha(CgState *cg, Gate g) {  // pq <= 0: break; alpha = rho/pq
+    if (gated(g)) return;
+    if (cg->pq <= 0.0)
+        cg->stop = 1;
+    else
+        cg->alpha = cg->rho / cg->pq;
+}
+__global__ void k_cg_beta(CgState *cg, Gate g) {  // rho_new == 0: break; p = r + (rho_new/rho) p
+    if (gated(g)) return;
+    if (cg->rho_new == 0.0) {
+        cg->stop = 1;
+    } else {
+        cg->beta = cg->rho_new / cg->rho;
+        cg->rho = cg->rho_new;
+    }
+}
+__global__ void k_cg_init(double *w, double *r, double *p, const double *u, int64_t s, Gate g) {
+    if (gated(g)) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+        w[i] = 0.0;
+        r[i] = u[i];
+        p[i] = u[i];
+    }
+}
+
+// ---- pcgls control (sv.py:184-241) ----
+__global__ void k_start_check(CglsState *st) {  // sv.py:184: z@z == 0 -> x = 0 stationary
+    st->iters_run = 0;
+    st->its_certified = 0;
+    st->hist_len = 0;
+    st->status = (st->zz == 0.0) ? ST_ZERO_START : ST_RUN;
+}
+__global__ void k_start_rho(CglsState *st, double *x_norms) {  // sv.py:198-199
+    if (st->status) return;
+    st->rho = st->zh;
+    x_norms[0] = 0.0;
+}
+__global__ void k_it_begin(CglsState *st) {  // need z@p only when rho <= 0 (sv.py:203)
+    if (st->status) return;
+    st->need_zp = !(st->rho > 0.0);
+}
+__global__ void k_it_sigma(CglsState *st) {  // sv.py:203-208
+    if (st->status) return;
+    st->sigma = st->rho > 0.0 ? st->rho : st->zp;
+    st->skip_retry = 1;
+    if (st->sigma == 0.0) {
+        st->skip_retry = 0;  // p = z.copy()
+        st->sigma = st->zz;  // float(z @ z): the same z whose z@z is stored
+        st->rho = st->sigma;
+    }
+}
+__global__ void k_it_alpha(CglsState *st) {  // sv.py:210-214
+    if (st->status) return;
+    if (st->qq <= 0.0 || st->sigma == 0.0)
+        st->status = ST_STOPPED;
+    else
+        st->alpha = st->sigma / st->qq;
+}
+__global__ void k_it_estimate(CglsState *st, double *alphas, double *sigmas, double *x_norms,
+                              double *history) {  // sv.py:217-232
+    if (st->status) return;
+    const long long it = st->iters_run;
+    alphas[it] = st->alpha;
+    sigmas[it] = st->sigma;
+    x_norms[it + 1] = st->xnorm;
+    st->iters_run = it + 1;
+    const long long i = st->iters_run - st->d;
+    if (i >= 0) {
+        const double estim = py_sum_products(alphas, sigmas, i, st->iters_run);
+        int err = 0;
+        const double ratio = py_stopping_ratio(estim, st->norm_A, x_norms[i], st->b_norm, st->ratio_raw, &err);
+        if (err) {
+            st->status = ST_ERROR;
+            return;
+        }
+        history[st->hist_len++] = ratio;
+        if (ratio <= st->delta) {
+            st->status = ST_CONVERGED;
+            st->its_certified = i;
+        }
+    }
+}
+__global__ void k_it_zz(CglsState *st) {  // sv.py:235-237
+    if (st->status) return;
+    if (st->zz == 0.0) st->status = ST_STOPPED;
+}
+__global__ void k_it_beta(CglsState *st) {  // sv.py:239-241
+    if (st->status) return;
+    const double rho_new = st->zh;
+    if (st->rho != 0.0) {
+        st->beta = rho_new / st->rho;
+        st->p_copy = 0;
+    } else {
+        st->p_copy = 1;
+    }
+    st->rho = rho_new;
+}
+__global__ void k_it_end(CglsState *st) {  // for-loop exhausted (sv.py:202)
+    if (st->status) return;
+    if (st->iters_run >= st->max_iters) st->status = ST_MAXED;
+}
+
+// ---- power method control (sc.py:439-454) ----
+__global__ void k_pm_start(PowerState *ps, int empty) {
+    ps->stop = 0;
+    ps->est = 0.0;
+    if (ps->nv == 0.0 || empty) {
+        ps->result = 0.0;
+        ps->stop = 1;
+    }
+}
+__global__ void k_pm_est(PowerState *ps) {
+    if (ps->stop) return;
+    if (ps->est == 0.0) {
+        ps->result = 0.0;
+        ps->stop = 1;
+    }
+}
+__global__ void k_pm_nt(PowerState *ps) {
+    if (ps->stop) return;
+    if (ps->nt == 0.0) {
+        ps->result = ps->est;
+        ps->stop = 1;
+    }
+}
+__global__ void k_pm_final(PowerState *ps) {
+    if (ps->stop) return;
+    ps->result = ps->est;
+}
+__global__ void k_div(double *dst, const double *src, const double *den, int64_t n, const int *stop) {
+    if (stop && *(volatile const int *)stop) return;
+    const double d = *den;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] / d;
+}
+
+inline int small_grid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+inline int chk(rsb_ctx *ctx, int kernels = 1) {
+    ctx->launches += kernels;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("kernel launch failed: %s", cudaGetErrorString(e));
+        return RSB_ECUDA;
+    }
+    return RSB_OK;
+}
+
+}  // namespace
+
+}  // namespace rsb
+
+using namespace rsb;
+
+// ---------------------------------------------------------------------------
+// preconditioner (pc.py:106-186)
+// ---------------------------------------------------------------------------
+struct rsb_pre {
+    rsb_ctx *ctx = nullptr;
+    int64_t m = 0, n = 0, s = 0;
+    int s_mode = 0, y_mode = 0, cg_iters = 0;
+    int32_t *perm = nullptr;  // device, length m
+    rsb_mat *L1 = nullptr, *L2 = nullptr, *U = nullptr, *Y = nullptr;
+    TriSched *tL1 = nullptr, *tL1T = nullptr, *tU = nullptr;
+    double *S = nullptr;  // s x s lower factor, column-major
+    // workspace
+    double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *v = nullptr;  // n
+    double *u = nullptr, *w = nullptr;                                  // s
+    double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;            // s
+    double *cg_a = nullptr, *cg_b = nullptr, *cg_c = nullptr;            // n
+    CgState *cg = nullptr;
+};
+
+namespace {
+
+// q = S p = p + L2 L1^{-1} L1^{-T} L2^T p  (s_matvec_implicit, pc.py:149-154)
+int enqueue_s_matvec(rsb_pre *P, const double *p, double *q, Gate g) {
+    rsb_ctx *ctx = P->ctx;
+    RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{p, nullptr, 0}, P->cg_a, EPI_STORE, VecIn{}, g));
+    RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->cg_a, nullptr, 0}, nullptr, P->cg_b, g));
+    RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{P->cg_b, nullptr, 0}, nullptr, P->cg_c, g));
+    RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->cg_c, nullptr, 0}, q, EPI_ADD, VecIn{p, nullptr, 0}, g));
+    return RSB_OK;
+}
+
+// w = _cg_fixed_steps(S, u, k)  (pc.py:284-310); returns the buffer holding w
+int enqueue_cg(rsb_pre *P, const double *u, Gate outer) {
+    rsb_ctx *ctx = P->ctx;
+    const int64_t s = P->s;
+    CgState *cg = P->cg;
+    k_cg_init<<<small_grid(s), 256, 0, ctx->stream>>>(P->w, P->cg_r, P->cg_p, u, s, outer);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_r, nullptr, 0}, VecIn{P->cg_r, nullptr, 0}, &cg->rho, 0, outer, nullptr));
+    k_cg_start<<<1, 1, 0, ctx->stream>>>(cg, outer);
+    RSB_TRY(chk(ctx));
+    Gate g{outer.a, &cg->stop};
+    for (int it = 0; it < P->cg_iters; ++it) {
+        RSB_TRY(enqueue_s_matvec(P, P->cg_p, P->cg_q, g));
+        RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_p, nullptr, 0}, VecIn{P->cg_q, nullptr, 0}, &cg->pq, 0, g, nullptr));
+        k_cg_alpha<<<1, 1, 0, ctx->stream>>>(cg, g);
+        RSB_TRY(chk(ctx));
+        RSB_TRY(launch_axpy(ctx, P->w, P->cg_p, &cg->alpha, +1, s, g));
+        RSB_TRY(launch_axpy(ctx, P->cg_r, P->cg_q, &cg->alpha, -1, s, g));
+        RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_r, nullptr, 0}, VecIn{P->cg_r, nullptr, 0}, &cg->rho_new, 0, g, nullptr));
+        k_cg_beta<<<1, 1, 0, ctx->stream>>>(cg, g);
+        RSB_TRY(chk(ctx));
+        RSB_TRY(launch_xpby(ctx, P->cg_p, P->cg_r, &cg->beta, nullptr, s, g));
+    }
+    return RSB_OK;
+}
+
+// h = apply(r1, r2)  (pc.py:175-186)
+int enqueue_apply(rsb_pre *P, VecIn r1, VecIn r2, double *h, Gate g) {
+    rsb_ctx *ctx = P->ctx;
+    if (P->s > 0) {
+        // u = r2 - Y r1
+        if (P->y_mode == RSB_Y_EXPLICIT) {
+            RSB_TRY(launch_spmv(ctx, P->Y->csr(), r1, P->u, EPI_SUB_FROM, r2, g));
+        } else {
+            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, P->t1, g));
+            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->t1, nullptr, 0}, P->u, EPI_SUB_FROM, r2, g));
+        }
+        // w = solve_S(u)
+        const double *w = P->w;
+        if (P->s_mode == RSB_S_DENSE) {
+            RSB_TRY(launch_chol_solve(ctx, P->S, P->s, P->u, P->w, g));
+        } else if (P->s_mode == RSB_S_IDENTITY) {
+            w = P->u;
+        } else {
+            RSB_TRY(enqueue_cg(P, P->u, g));
+        }
+        // y = r1 + Y^T w ; v = L1^{-1} y
+        if (P->y_mode == RSB_Y_EXPLICIT) {
+            RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{w, nullptr, 0}, P->t3, EPI_ADD, r1, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{P->t3, nullptr, 0}, nullptr, P->v, g));
+        } else {
+            RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{w, nullptr, 0}, P->t2, EPI_STORE, VecIn{}, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->t2, nullptr, 0}, nullptr, P->t3, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, P->t3, P->v, g));
+        }
+    } else {
+        RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, P->v, g));
+    }
+    return launch_trsv(ctx, *P->tU, VecIn{P->v, nullptr, 0}, nullptr, h, g);
+}
+
+void pre_free(rsb_pre *P) {
+    rsb_ctx *ctx = P->ctx;
+    const size_t n8 = P->n * sizeof(double), s8 = P->s * sizeof(double);
+    dev_free(ctx, P->perm, P->m * sizeof(int32_t));
+    if (P->S) dev_free(ctx, P->S, P->s * P->s * sizeof(double));
+    for (double *q : {P->t1, P->t2, P->t3, P->v, P->cg_a, P->cg_b, P->cg_c}) dev_free(ctx, q, n8);
+    for (double *q : {P->u, P->w, P->cg_r, P->cg_p, P->cg_q}) dev_free(ctx, q, s8);
+    dev_free(ctx, P->cg, sizeof(CgState));
+    delete P;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// solver (sv.py:120-268)
+// ---------------------------------------------------------------------------
+struct rsb_solver {
+    rsb_ctx *ctx = nullptr;
+    rsb_mat *A = nullptr;
+    rsb_pre *pre = nullptr;
+    int64_t m = 0, n = 0;
+    double *b = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *fr = nullptr;  // m: b, r, q, fr
+    double *z = nullptr, *h = nullptr, *p = nullptr, *g = nullptr;                 // n
+    CglsState *st = nullptr;
+    CglsState *h_st = nullptr;  // pinned mirror
+    double *alphas = nullptr, *sigmas = nullptr, *x_norms = nullptr, *history = nullptr;
+    int64_t cap = 0;  // capacity of the per-iteration arrays (max_iters)
+    int d = 5;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t graph_kernels = 0;
+    bool started = false;
+    rsb_cgls_cfg cfg{};
+};
+
+namespace {
+
+int enqueue_precondition(rsb_solver *S, Gate g) {
+    if (S->pre) {
+        const rsb_pre *P = S->pre;
+        return enqueue_apply(S->pre, VecIn{S->r, P->perm, 0}, VecIn{S->r, P->perm, S->n}, S->h, g);
+    }
+    return launch_copy(S->ctx, S->h, VecIn{S->z, nullptr, 0}, S->n, g);  // h = A^T r (sv.py:166-167)
+}
+
+// one iteration of sv.py:202-241
+int enqueue_iteration(rsb_solver *S) {
+    rsb_ctx *ctx = S->ctx;
+    CglsState *st = S->st;
+    const Gate g{&st->status, nullptr};
+    const int64_t m = S->m, n = S->n;
+    k_it_begin<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->p, nullptr, 0}, &st->zp, 0, g, &st->need_zp));
+    k_it_sigma<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_copy(ctx, S->p, VecIn{S->z, nullptr, 0}, n, Gate{&st->status, &st->skip_retry}));
+    RSB_TRY(launch_spmv(ctx, S->A->csr(), VecIn{S->p, nullptr, 0}, S->q, EPI_STORE, VecIn{}, g));
+    RSB_TRY(launch_dot(ctx, m, VecIn{S->q, nullptr, 0}, VecIn{S->q, nullptr, 0}, &st->qq, 0, g, nullptr));
+    k_it_alpha<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_axpy(ctx, S->x, S->p, &st->alpha, +1, n, g));
+    RSB_TRY(launch_axpy(ctx, S->r, S->q, &st->alpha, -1, m, g));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->x, nullptr, 0}, VecIn{S->x, nullptr, 0}, &st->xnorm, 1, g, nullptr));
+    k_it_estimate<<<1, 1, 0, ctx->stream>>>(st, S->alphas, S->sigmas, S->x_norms, S->history);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_spmv_t(ctx, S->A->csc(), VecIn{S->r, nullptr, 0}, S->z, EPI_STORE, VecIn{}, g));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->z, nullptr, 0}, &st->zz, 0, g, nullptr));
+    k_it_zz<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(enqueue_precondition(S, g));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->h, nullptr, 0}, &st->zh, 0, g, nullptr));
+    k_it_beta<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_xpby(ctx, S->p, S->h, &st->beta, &st->p_copy, n, g));
+    k_it_end<<<1, 1, 0, ctx->stream>>>(st);
+    return chk(ctx);
+}
+
+int ensure_capacity(rsb_solver *S, int64_t max_iters, int d) {
+    if (max_iters <= S->cap && d <= S->d && S->exec) return RSB_OK;
+    rsb_ctx *ctx = S->ctx;
+    cudaStreamSynchronize(ctx->stream);
+    if (S->exec) {
+        cudaGraphExecDestroy(S->exec);
+        cudaGraphDestroy(S->graph);
+        S->exec = nullptr;
+        S->graph = nullptr;
+    }
+    if (max_iters > S->cap || d > S->d) {
+        const int64_t cap = std::max(max_iters, S->cap);
+        const int dd = std::max(d, S->d);
+        dev_free(ctx, S->alphas, S->cap * sizeof(double));
+        dev_free(ctx, S->sigmas, S->cap * sizeof(double));
+        dev_free(ctx, S->x_norms, (S->cap + 1) * sizeof(double));
+        dev_free(ctx, S->history, (S->cap + S->d + 1) * sizeof(double));
+        S->cap = cap;
+        S->d = dd;
+        RSB_TRY(dev_alloc(ctx, (void **)&S->alphas, cap * sizeof(double)));
+        RSB_TRY(dev_alloc(ctx, (void **)&S->sigmas, cap * sizeof(double)));
+        RSB_TRY(dev_alloc(ctx, (void **)&S->x_norms, (cap + 1) * sizeof(double)));
+        RSB_TRY(dev_alloc(ctx, (void **)&S->history, (cap + dd + 1) * sizeof(double)));
+    }
+    // capture one iteration as a graph
+    const int64_t before = ctx->launches;
+    RSB_TRY_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_iteration(S);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (rc != RSB_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    RSB_TRY_CUDA(e);
+    S->graph = graph;
+    RSB_TRY_CUDA(cudaGraphInstantiate(&S->exec, graph, 0));
+    S->graph_kernels = ctx->launches - before;
+    ctx->launches = before;
+    return RSB_OK;
+}
+
+int read_state(rsb_solver *S) {
+    rsb_ctx *ctx = S->ctx;
+    RSB_TRY_CUDA(cudaMemcpyAsync(S->h_st, S->st, sizeof(CglsState), cudaMemcpyDeviceToHost, ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RSB_OK;
+}
+
+void solver_free(rsb_solver *S) {
+    rsb_ctx *ctx = S->ctx;
+    cudaStreamSynchronize(ctx->stream);
+    if (S->exec) cudaGraphExecDestroy(S->exec);
+    if (S->graph) cudaGraphDestroy(S->graph);
+    const size_t m8 = S->m * sizeof(double), n8 = S->n * sizeof(double);
+    for (double *q : {S->b, S->r, S->q, S->fr}) dev_free(ctx, q, m8);
+    for (double *q : {S->x, S->z, S->h, S->p, S->g}) dev_free(ctx, q, n8);
+    dev_free(ctx, S->st, sizeof(CglsState));
+    if (S->h_st) cudaFreeHost(S->h_st);
+    dev_free(ctx, S->alphas, S->cap * sizeof(double));
+    dev_free(ctx, S->sigmas, S->cap * sizeof(double));
+    dev_free(ctx, S->x_norms, (S->cap + 1) * sizeof(double));
+    dev_free(ctx, S->history, (S->cap + S->d + 1) * sizeof(double));
+    delete S;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsb_pre_create(rsb_ctx *ctx, int64_t m, int64_t n, const int64_t *perm, rsb_mat *L1, rsb_mat *L2,
+                   rsb_mat *U, rsb_mat *Y, const double *S_factor, int64_t s, int s_mode, int y_mode,
+                   int cg_iters, rsb_pre **out) {
+    *out = nullptr;
+    if (cg_iters < 1) {
+        set_error("cg_iters must be >= 1");
+        return RSB_EINVAL;
+    }
+    if (s_mode < 0 || s_mode > 2 || y_mode < 0 || y_mode > 1) {
+        set_error("unknown s_mode/y_mode");
+        return RSB_EINVAL;
+    }
+    if (s_mode == RSB_S_DENSE && y_mode != RSB_Y_EXPLICIT) {
+        set_error("dense S factorization requires the explicit Y");
+        return RSB_EINVAL;
+    }
+    if (!L1 || !L2 || !U || L1->nrows != n || L1->ncols != n || U->nrows != n || U->ncols != n ||
+        L2->ncols != n || L2->nrows != s || m != n + s) {
+        set_error("inconsistent factor dimensions");
+        return RSB_EINVAL;
+    }
+    if (y_mode == RSB_Y_EXPLICIT && (!Y || Y->nrows != s || Y->ncols != n)) {
+        set_error("explicit Y mode needs Y of shape (%lld, %lld)", (long long)s, (long long)n);
+        return RSB_EINVAL;
+    }
+    if (s_mode == RSB_S_DENSE && s > 0 && !S_factor) {
+        set_error("dense S mode needs the S factor");
+        return RSB_EINVAL;
+    }
+    for (int64_t i = 0; i < m; ++i)
+        if (perm[i] < 0 || perm[i] >= m) {
+            set_error("row permutation entry out of range");
+            return RSB_EINVAL;
+        }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    auto *P = new rsb_pre();
+    P->ctx = ctx;
+    P->m = m;
+    P->n = n;
+    P->s = s;
+    P->s_mode = s_mode;
+    P->y_mode = y_mode;
+    P->cg_iters = cg_iters;
+    P->L1 = L1;
+    P->L2 = L2;
+    P->U = U;
+    P->Y = Y;
+    int rc = RSB_OK;
+    std::vector<int32_t> pm(perm, perm + m);
+    const size_t n8 = n * sizeof(double), s8 = s * sizeof(double);
+#define PTRY(x)                 \
+    if ((rc = (x)) != RSB_OK) { \
+        pre_free(P);            \
+        return rc;              \
+    }
+    PTRY(get_tri(L1, RSB_TRI_LOWER_UNIT, &P->tL1));
+    PTRY(get_tri(U, RSB_TRI_UPPER, &P->tU));
+    if (s > 0 && (y_mode == RSB_Y_IMPLICIT || s_mode == RSB_S_CG)) PTRY(get_tri(L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
+    PTRY(dev_upload(ctx, &P->perm, pm.data(), pm.size()));
+    if (s_mode == RSB_S_DENSE && s > 0) {
+        PTRY(dev_upload(ctx, &P->S, S_factor, (size_t)(s * s)));
+        PTRY(prepare_chol(s));
+    }
+    for (double **q : {&P->t1, &P->t2, &P->t3, &P->v, &P->cg_a, &P->cg_b, &P->cg_c}) PTRY(dev_alloc(ctx, (void **)q, n8));
+    for (double **q : {&P->u, &P->w, &P->cg_r, &P->cg_p, &P->cg_q}) PTRY(dev_alloc(ctx, (void **)q, s8));
+    PTRY(dev_alloc(ctx, (void **)&P->cg, sizeof(CgState)));
+#undef PTRY
+    RSB_TRY_CUDA(cudaMemsetAsync(P->cg, 0, sizeof(CgState), ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = P;
+    return RSB_OK;
+}
+
+int rsb_pre_destroy(rsb_pre *pre) {
+    if (!pre) return RSB_OK;
+    cudaStreamSynchronize(pre->ctx->stream);
+    pre_free(pre);
+    return RSB_OK;
+}
+
+int rsb_pre_apply(rsb_pre *P, const double *r1, const double *r2, double *h, int where) {
+    rsb_ctx *ctx = P->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged s1, s2, sh;
+    RSB_TRY(stage_in(ctx, r1, P->n, where, s1));
+    RSB_TRY(stage_in(ctx, r2, P->s, where, s2));
+    RSB_TRY(stage_out(ctx, h, P->n, where, sh));
+    RSB_TRY(enqueue_apply(P, VecIn{s1.d, nullptr, 0}, VecIn{s2.d, nullptr, 0}, sh.d, Gate{}));
+    return finish_out(ctx, h, P->n, where, sh);
+}
+
+int rsb_pre_y_apply(rsb_pre *P, const double *r1, double *out, int where) {
+    rsb_ctx *ctx = P->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged s1, so;
+    RSB_TRY(stage_in(ctx, r1, P->n, where, s1));
+    RSB_TRY(stage_out(ctx, out, P->s, where, so));
+    if (P->s > 0) {
+        if (P->y_mode == RSB_Y_EXPLICIT) {
+            RSB_TRY(launch_spmv(ctx, P->Y->csr(), VecIn{s1.d, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
+        } else {
+            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{s1.d, nullptr, 0}, nullptr, P->t1, Gate{}));
+            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->t1, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
+        }
+    }
+    return finish_out(ctx, out, P->s, where, so);
+}
+
+int rsb_pre_y_apply_transpose(rsb_pre *P, const double *w, double *out, int where) {
+    rsb_ctx *ctx = P->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged sw, so;
+    RSB_TRY(stage_in(ctx, w, P->s, where, sw));
+    RSB_TRY(stage_out(ctx, out, P->n, where, so));
+    if (P->y_mode == RSB_Y_EXPLICIT) {
+        RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{sw.d, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
+    } else {
+        if (!P->tL1T) RSB_TRY(get_tri(P->L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
+        RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{sw.d, nullptr, 0}, P->t2, EPI_STORE, VecIn{}, Gate{}));
+        RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->t2, nullptr, 0}, nullptr, so.d, Gate{}));
+    }
+    return finish_out(ctx, out, P->n, where, so);
+}
+
+int rsb_pre_s_matvec(rsb_pre *P, const double *v, double *out, int where) {
+    rsb_ctx *ctx = P->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    Staged sv, so;
+    RSB_TRY(stage_in(ctx, v, P->s, where, sv));
+    RSB_TRY(stage_out(ctx, out, P->s, where, so));
+    if (P->s > 0) {
+        if (!P->tL1T) RSB_TRY(get_tri(P->L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
+        RSB_TRY(enqueue_s_matvec(P, sv.d, so.d, Gate{}));
+    }
+    return finish_out(ctx, out, P->s, where, so);
+}
+
+int rsb_solver_create(rsb_mat *A, rsb_pre *pre, rsb_solver **out) {
+    *out = nullptr;
+    rsb_ctx *ctx = A->ctx;
+    if (pre && (pre->m != A->nrows || pre->n != A->ncols)) {
+        set_error("preconditioner does not match the matrix");
+        return RSB_EINVAL;
+    }
+    if (pre && pre->ctx != ctx) {
+        set_error("matrix and preconditioner belong to different contexts");
+        return RSB_EINVAL;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    auto *S = new rsb_solver();
+    S->ctx = ctx;
+    S->A = A;
+    S->pre = pre;
+    S->m = A->nrows;
+    S->n = A->ncols;
+    int rc = RSB_OK;
+    const size_t m8 = S->m * sizeof(double), n8 = S->n * sizeof(double);
+    for (double **q : {&S->b, &S->r, &S->q, &S->fr})
+        if ((rc = dev_alloc(ctx, (void **)q, m8)) != RSB_OK) break;
+    for (double **q : {&S->x, &S->z, &S->h, &S->p, &S->g})
+        if (rc == RSB_OK) rc = dev_alloc(ctx, (void **)q, n8);
+    if (rc == RSB_OK) rc = dev_alloc(ctx, (void **)&S->st, sizeof(CglsState));
+    if (rc == RSB_OK && cudaMallocHost((void **)&S->h_st, sizeof(CglsState)) != cudaSuccess) {
+        set_error("pinned allocation failed");
+        rc = RSB_ENOMEM;
+    }
+    if (rc != RSB_OK) {
+        solver_free(S);
+        return rc;
+    }
+    *out = S;
+    return RSB_OK;
+}
+
+int rsb_solver_destroy(rsb_solver *S) {
+    if (S) solver_free(S);
+    return RSB_OK;
+}
+
+int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, int *status) {
+    rsb_ctx *ctx = S->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    if (!(cfg->delta > 0.0) || cfg->estimator_delay < 1 || cfg->max_iters < 1) {
+        set_error("invalid CglsConfig (delta > 0, estimator_delay >= 1, max_iters >= 1)");
+        return RSB_EINVAL;
+    }
+    RSB_TRY(ensure_capacity(S, cfg->max_iters, cfg->estimator_delay));
+    S->cfg = *cfg;
+    const int64_t m = S->m, n = S->n;
+    if (where == RSB_DEVICE) {
+        RSB_TRY_CUDA(cudaMemcpyAsync(S->b, b, m * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+        RSB_TRY_CUDA(cudaMemcpyAsync(S->b, b, m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CglsState init{};
+    init.norm_A = cfg->norm_A;
+    init.delta = cfg->delta;
+    init.max_iters = cfg->max_iters;
+    init.d = cfg->estimator_delay;
+    init.ratio_raw = cfg->ratio_raw;
+    *S->h_st = init;
+    RSB_TRY_CUDA(cudaMemcpyAsync(S->st, S->h_st, sizeof(CglsState), cudaMemcpyHostToDevice, ctx->stream));
+    CglsState *st = S->st;
+    const Gate none{};
+    const Gate g{&st->status, nullptr};
+    // sv.py:152, 171-173
+    RSB_TRY(launch_dot(ctx, m, VecIn{S->b, nullptr, 0}, VecIn{S->b, nullptr, 0}, &st->b_norm, 1, none, nullptr));
+    RSB_TRY(launch_fill(ctx, S->x, n, 0ull, none));
+    RSB_TRY(launch_copy(ctx, S->r, VecIn{S->b, nullptr, 0}, m, none));
+    RSB_TRY(launch_spmv_t(ctx, S->A->csc(), VecIn{S->r, nullptr, 0}, S->z, EPI_STORE, VecIn{}, none));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->z, nullptr, 0}, &st->zz, 0, none, nullptr));
+    k_start_check<<<1, 1, 0, ctx->stream>>>(st);
+    RSB_TRY(chk(ctx));
+    // sv.py:198-200
+    RSB_TRY(enqueue_precondition(S, g));
+    RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->h, nullptr, 0}, &st->zh, 0, g, nullptr));
+    k_start_rho<<<1, 1, 0, ctx->stream>>>(st, S->x_norms);
+    RSB_TRY(chk(ctx));
+    RSB_TRY(launch_copy(ctx, S->p, VecIn{S->h, nullptr, 0}, n, g));
+    RSB_TRY(read_state(S));
+    if (S->h_st->status == ST_ERROR) {
+        set_error("zero denominator in stopping ratio");
+        return RSB_EINVAL;
+    }
+    S->started = true;
+    *status = S->h_st->status;
+    return RSB_OK;
+}
+
+int rsb_solver_iterate(rsb_solver *S, int64_t k, int64_t *iters_run, int *status) {
+    rsb_ctx *ctx = S->ctx;
+    if (!S->started) {
+        set_error("rsb_solver_iterate before rsb_solver_start");
+        return RSB_ESTATE;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    int64_t done = 0;
+    int st = S->h_st->status;
+    // batches of graph replays; kernels are gated on the device status, so
+    // replays past a stop are no-ops
+    int64_t batch = 4;
+    while (st == ST_RUN && done < k) {
+        const int64_t nb = std::min(batch, k - done);
+        for (int64_t i = 0; i < nb; ++i) RSB_TRY_CUDA(cudaGraphLaunch(S->exec, ctx->stream));
+        ctx->launches += nb * S->graph_kernels;
+        done += nb;
+        RSB_TRY(read_state(S));
+        st = S->h_st->status;
+        batch = std::min<int64_t>(batch * 2, 64);
+    }
+    if (st == ST_ERROR) {
+        set_error("zero denominator in stopping ratio");
+        return RSB_EINVAL;
+    }
+    *iters_run = S->h_st->iters_run;
+    *status = st;
+    return RSB_OK;
+}
+
+int rsb_solver_get_x(rsb_solver *S, double *x, int where) {
+    rsb_ctx *ctx = S->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    RSB_TRY_CUDA(cudaMemcpyAsync(x, S->x, S->n * sizeof(double),
+                                 where == RSB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+    return RSB_OK;
+}
+
+int rsb_solver_finish(rsb_solver *S, rsb_report *rep, double *history, int64_t history_cap) {
+    rsb_ctx *ctx = S->ctx;
+    if (!S->started) {
+        set_error("rsb_solver_finish before rsb_solver_start");
+        return RSB_ESTATE;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    RSB_TRY(read_state(S));
+    const CglsState st = *S->h_st;
+    std::memset(rep, 0, sizeof *rep);
+    if (st.status == ST_ZERO_START) {  // sv.py:184-196
+        rep->its = 0;
+        rep->converged = 1;
+        rep->breakdown = 0;
+        rep->ratio_pt_final = 0.0;
+        rep->residual_norm = st.b_norm;
+        rep->gradient_norm = 0.0;
+        rep->history_len = 1;
+        if (history_cap > 0) history[0] = 0.0;
+        return RSB_OK;
+    }
+    const long long it_run = st.iters_run;
+    std::vector<double> al(it_run), sg(it_run), xn(it_run + 1), hist(st.hist_len);
+    if (it_run) {
+        RSB_TRY_CUDA(cudaMemcpyAsync(al.data(), S->alphas, it_run * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        RSB_TRY_CUDA(cudaMemcpyAsync(sg.data(), S->sigmas, it_run * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    RSB_TRY_CUDA(cudaMemcpyAsync(xn.data(), S->x_norms, (it_run + 1) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (st.hist_len)
+        RSB_TRY_CUDA(cudaMemcpyAsync(hist.data(), S->history, st.hist_len * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    // final residual and gradient (sv.py:256-266), enqueued before the sync
+    CglsState *dst = S->st;
+    RSB_TRY(launch_spmv(ctx, S->A->csr(), VecIn{S->x, nullptr, 0}, S->fr, EPI_SUB_FROM, VecIn{S->b, nullptr, 0}, Gate{}));
+    RSB_TRY(launch_dot(ctx, S->m, VecIn{S->fr, nullptr, 0}, VecIn{S->fr, nullptr, 0}, &dst->qq, 1, Gate{}, nullptr));
+    RSB_TRY(launch_spmv_t(ctx, S->A->csc(), VecIn{S->fr, nullptr, 0}, S->g, EPI_STORE, VecIn{}, Gate{}));
+    RSB_TRY(launch_dot(ctx, S->n, VecIn{S->g, nullptr, 0}, VecIn{S->g, nullptr, 0}, &dst->zz, 1, Gate{}, nullptr));
+    RSB_TRY(read_state(S));
+    const double res_norm = S->h_st->qq, grad_norm = S->h_st->zz;
+
+    bool converged = st.status == ST_CONVERGED;
+    const bool stopped_early = st.status == ST_STOPPED;
+    long long its_cert = st.its_certified;
+    if (stopped_early && !converged) {  // sv.py:243-253
+        const int d = S->cfg.estimator_delay;
+        for (long long i = std::max(0LL, it_run - d + 1); i <= it_run; ++i) {
+            const double estim = py_sum_products(al.data(), sg.data(), i, it_run);
+            int err = 0;
+            const double ratio = py_stopping_ratio(estim, S->cfg.norm_A, xn[i], st.b_norm, S->cfg.ratio_raw, &err);
+            if (err) {
+                set_error("zero denominator in stopping ratio");
+                return RSB_EINVAL;
+            }
+            hist.push_back(ratio);
+            if (ratio <= S->cfg.delta) {
+                converged = true;
+                its_cert = i;
+                break;
+            }
+        }
+    }
+    rep->iters_run = it_run;
+    rep->its = converged ? its_cert : it_run;
+    rep->converged = converged;
+    rep->breakdown = stopped_early && !converged;
+    rep->ratio_pt_final = hist.empty() ? INFINITY : hist.back();
+    rep->residual_norm = res_norm;
+    rep->gradient_norm = grad_norm;
+    rep->history_len = (int64_t)hist.size();
+    for (int64_t i = 0; i < std::min<int64_t>(history_cap, (int64_t)hist.size()); ++i) history[i] = hist[i];
+    return RSB_OK;
+}
+
+int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, double *x, rsb_report *rep,
+              double *history, int64_t history_cap) {
+    int status = 0;
+    RSB_TRY(rsb_solver_start(S, b, where, cfg, &status));
+    if (status == ST_RUN) {
+        int64_t iters = 0;
+        RSB_TRY(rsb_solver_iterate(S, cfg->max_iters, &iters, &status));
+    }
+    RSB_TRY(rsb_solver_finish(S, rep, history, history_cap));
+    return rsb_solver_get_x(S, x, where);
+}
+
+// power_method_norm2 (sc.py:428-454); v0 drawn on the host
+int rsb_power_norm2(rsb_mat *A, const double *v0, int iters, double *est) {
+    rsb_ctx *ctx = A->ctx;
+    if (iters < 1) {
+        set_error("iters must be >= 1");
+        return RSB_EINVAL;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    const int64_t m = A->nrows, n = A->ncols;
+    double *v = nullptr, *w = nullptr;
+    PowerState *ps = nullptr;
+    int rc = RSB_OK;
+    if ((rc = dev_alloc(ctx, (void **)&v, n * sizeof(double))) != RSB_OK) return rc;
+    if ((rc = dev_alloc(ctx, (void **)&w, m * sizeof(double))) != RSB_OK) {
+        dev_free(ctx, v, n * sizeof(double));
+        return rc;
+    }
+    if ((rc = dev_alloc(ctx, (void **)&ps, sizeof(PowerState))) != RSB_OK) {
+        dev_free(ctx, v, n * sizeof(double));
+        dev_free(ctx, w, m * sizeof(double));
+        return rc;
+    }
+    auto run = [&]() -> int {
+        RSB_TRY_CUDA(cudaMemcpyAsync(v, v0, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        RSB_TRY(launch_dot(ctx, n, VecIn{v, nullptr, 0}, VecIn{v, nullptr, 0}, &ps->nv, 1, Gate{}, nullptr));
+        k_pm_start<<<1, 1, 0, ctx->stream>>>(ps, A->nnz == 0);
+        RSB_TRY(chk(ctx));
+        k_div<<<small_grid(n), 256, 0, ctx->stream>>>(v, v, &ps->nv, n, &ps->stop);
+        RSB_TRY(chk(ctx));
+        const Gate g{&ps->stop, nullptr};
+        // the `t` of sc.py:449 reuses the n-vector v once v is consumed
+        for (int it = 0; it < iters; ++it) {
+            RSB_TRY(launch_spmv(ctx, A->csr(), VecIn{v, nullptr, 0}, w, EPI_STORE, VecIn{}, g));
+            RSB_TRY(launch_dot(ctx, m, VecIn{w, nullptr, 0}, VecIn{w, nullptr, 0}, &ps->est, 1, g, nullptr));
+            k_pm_est<<<1, 1, 0, ctx->stream>>>(ps);
+            RSB_TRY(chk(ctx));
+            RSB_TRY(launch_spmv_t(ctx, A->csc(), VecIn{w, nullptr, 0}, v, EPI_STORE, VecIn{}, g));
+            RSB_TRY(launch_dot(ctx, n, VecIn{v, nullptr, 0}, VecIn{v, nullptr, 0}, &ps->nt, 1, g, nullptr));
+            k_pm_nt<<<1, 1, 0, ctx->stream>>>(ps);
+            RSB_TRY(chk(ctx));
+            k_div<<<small_grid(n), 256, 0, ctx->stream>>>(v, v, &ps->nt, n, &ps->stop);
+            RSB_TRY(chk(ctx));
+        }
+        k_pm_final<<<1, 1, 0, ctx->stream>>>(ps);
+        RSB_TRY(chk(ctx));
+        RSB_TRY_CUDA(cudaMemcpyAsync(ctx->h_scalar, &ps->result, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
+        *est = ctx->h_scalar[0];
+        return RSB_OK;
+    };
+    rc = run();
+    cudaStreamSynchronize(ctx->stream);
+    dev_free(ctx, v, n * sizeof(double));
+    dev_free(ctx, w, m * sizeof(double));
+    dev_free(ctx, ps, sizeof(PowerState));
+    return rc;
+}
+
+}  // extern "C"
