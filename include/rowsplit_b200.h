@@ -168,6 +168,14 @@ int rsb_solver_get_x(rsb_solver *S, double *x, int where);
 /* partial-window certification, final residual and gradient norms
  * (sv.py:243-266); history gets min(cap, history_len) ratios. */
 int rsb_solver_finish(rsb_solver *S, rsb_report *rep, double *history, int64_t history_cap);
+/* Measurement: k iterations, each a replay of an instrumented copy of the
+ * iteration graph bracketed by CUDA events on the context stream (L2 flushed
+ * before each when flush != 0, outside the bracket).  Outputs the summed
+ * device ms of the iterations and of the triangular solves inside them. */
+int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, double *tri_ms,
+                     int64_t *tri_launches, int64_t *kernels_per_iter, int *status);
+/* overwrite a 320 MiB scratch buffer (> L2) on the context stream */
+int rsb_l2_flush(rsb_ctx *ctx);
 /* whole solve in one call: start + iterate + finish + get_x */
 int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, double *x,
               rsb_report *rep, double *history, int64_t history_cap);

@@ -83,6 +83,8 @@ _SIGS = {
     "rsb_solver_get_x": [vp, vp, ctypes.c_int],
     "rsb_solver_finish": [vp, ctypes.POINTER(ReportC), vp, i64],
     "rsb_pcgls": [vp, vp, ctypes.c_int, ctypes.POINTER(CglsCfgC), vp, ctypes.POINTER(ReportC), vp, i64],
+    "rsb_solver_bench": [vp, i64, ctypes.c_int, f64p, f64p, i64p, i64p, ctypes.POINTER(ctypes.c_int)],
+    "rsb_l2_flush": [vp],
     "rsb_ilup_factorize": [i64, i64, vp, vp, vp, i64, f64, f64, f64, ctypes.POINTER(vp)],
     "rsb_ilup_sizes": [vp, i64p, i64p, i64p, i64p],
     "rsb_ilup_copy": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],

@@ -134,6 +134,7 @@ int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
     ctx->flags = flags;
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     for (int i = 0; e == cudaSuccess && i < 16; ++i) e = cudaEventCreate(&ctx->ev[i]);
+    for (int i = 0; e == cudaSuccess && i < 64; ++i) e = cudaEventCreate(&ctx->trace_ev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&ctx->h_scalar, 64 * sizeof(double));
     if (e != cudaSuccess) {
         set_error("context setup failed: %s", cudaGetErrorString(e));
@@ -162,6 +163,9 @@ int rsb_ctx_destroy(rsb_ctx *ctx) {
     if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : ctx->trace_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->flush_buf) dev_free(ctx, ctx->flush_buf, ctx->flush_bytes);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return RSB_OK;
@@ -205,6 +209,11 @@ int rsb_memcpy(rsb_ctx *ctx, void *dst, const void *src, int64_t bytes, int kind
     cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     RSB_TRY_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, k, ctx->stream));
     return RSB_OK;
+}
+
+int rsb_l2_flush(rsb_ctx *ctx) {
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    return launch_l2_flush(ctx);
 }
 
 int rsb_event_mark(rsb_ctx *ctx, int slot) {

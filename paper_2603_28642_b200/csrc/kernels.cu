@@ -417,6 +417,9 @@ int launch_fill(rsb_ctx *ctx, double *x, int64_t n, unsigned long long bits, Gat
 
 int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g) {
     if (T.n == 0) return RSB_OK;
+    const bool trace = ctx->tracing && ctx->trace_n + 2 <= 64;
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
     RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
     const int grid = grid_for(T.n, kTriBlock);
     const TriDev v = T.view();
@@ -426,6 +429,26 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         case 2: k_trsv<2><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
         default: k_trsv<3><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
     }
+    RSB_TRY(post_launch(ctx));
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
+    return RSB_OK;
+}
+
+namespace {
+__global__ void k_flush(double *buf, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        buf[i] = (double)i;
+}
+}  // namespace
+
+int launch_l2_flush(rsb_ctx *ctx) {
+    const size_t bytes = 320ull << 20;  // > 2.5x the 126 MB L2
+    if (!ctx->flush_buf) {
+        RSB_TRY(dev_alloc(ctx, &ctx->flush_buf, bytes));
+        ctx->flush_bytes = bytes;
+    }
+    k_flush<<<148 * 8, kBlock, 0, ctx->stream>>>((double *)ctx->flush_buf, (int64_t)(bytes / 8));
     return post_launch(ctx);
 }
 

@@ -129,6 +129,14 @@ struct rsb_ctx {
     // tree-dot partials
     double *d_partials = nullptr;
     int partial_cap = 0;
+    // bench instrumentation: event-record nodes around every triangular
+    // solve captured into an instrumented iteration graph
+    bool tracing = false;
+    int trace_n = 0;
+    cudaEvent_t trace_ev[64] = {};
+    // L2 flush buffer (bench only, allocated on first use)
+    void *flush_buf = nullptr;
+    size_t flush_bytes = 0;
 };
 
 struct rsb_mat {
@@ -207,6 +215,8 @@ int launch_axpy(rsb_ctx *ctx, double *y, const double *x, const double *scal, in
 // p = h + (*beta) * p, or p = h when *copy_flag != 0
 int launch_xpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, const int *copy_flag,
                 int64_t n, Gate g);
+// overwrite a buffer larger than L2 (bench: cold-cache iterations)
+int launch_l2_flush(rsb_ctx *ctx);
 // dense Cholesky solve with the lower column-major factor (sc.py:607-622)
 int launch_chol_solve(rsb_ctx *ctx, const double *G, int64_t s, const double *u, double *w, Gate g);
 

@@ -365,6 +365,11 @@ struct rsb_solver {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t graph_kernels = 0;
+    // instrumented copy of the iteration graph (bench): event-record nodes
+    // around every triangular solve
+    cudaGraph_t bgraph = nullptr;
+    cudaGraphExec_t bexec = nullptr;
+    int btrace = 0;
     bool started = false;
     rsb_cgls_cfg cfg{};
 };
@@ -423,6 +428,12 @@ int ensure_capacity(rsb_solver *S, int64_t max_iters, int d) {
         S->exec = nullptr;
         S->graph = nullptr;
     }
+    if (S->bexec) {
+        cudaGraphExecDestroy(S->bexec);
+        cudaGraphDestroy(S->bgraph);
+        S->bexec = nullptr;
+        S->bgraph = nullptr;
+    }
     if (max_iters > S->cap || d > S->d) {
         const int64_t cap = std::max(max_iters, S->cap);
         const int dd = std::max(d, S->d);
@@ -467,6 +478,8 @@ void solver_free(rsb_solver *S) {
     cudaStreamSynchronize(ctx->stream);
     if (S->exec) cudaGraphExecDestroy(S->exec);
     if (S->graph) cudaGraphDestroy(S->graph);
+    if (S->bexec) cudaGraphExecDestroy(S->bexec);
+    if (S->bgraph) cudaGraphDestroy(S->bgraph);
     const size_t m8 = S->m * sizeof(double), n8 = S->n * sizeof(double);
     for (double *q : {S->b, S->r, S->q, S->fr}) dev_free(ctx, q, m8);
     for (double *q : {S->x, S->z, S->h, S->p, S->g}) dev_free(ctx, q, n8);
@@ -820,6 +833,62 @@ int rsb_solver_finish(rsb_solver *S, rsb_report *rep, double *history, int64_t h
     rep->gradient_norm = grad_norm;
     rep->history_len = (int64_t)hist.size();
     for (int64_t i = 0; i < std::min<int64_t>(history_cap, (int64_t)hist.size()); ++i) history[i] = hist[i];
+    return RSB_OK;
+}
+
+// Bench: k iterations, each one replay of the instrumented iteration graph
+// bracketed by events, optionally preceded by an L2 flush that is outside
+// the bracket.  Returns the summed device time of the iterations and of the
+// triangular solves inside them.
+int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, double *tri_ms,
+                     int64_t *tri_launches, int64_t *kernels_per_iter, int *status) {
+    rsb_ctx *ctx = S->ctx;
+    if (!S->started) {
+        set_error("rsb_solver_bench before rsb_solver_start");
+        return RSB_ESTATE;
+    }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    if (!S->bexec) {
+        ctx->tracing = true;
+        ctx->trace_n = 0;
+        const int64_t before = ctx->launches;
+        RSB_TRY_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_iteration(S);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        ctx->tracing = false;
+        ctx->launches = before;
+        if (rc != RSB_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        RSB_TRY_CUDA(e);
+        S->bgraph = graph;
+        RSB_TRY_CUDA(cudaGraphInstantiate(&S->bexec, graph, 0));
+        S->btrace = ctx->trace_n;
+    }
+    double it_total = 0.0, tri_total = 0.0;
+    for (int64_t i = 0; i < k; ++i) {
+        if (flush) RSB_TRY(launch_l2_flush(ctx));
+        RSB_TRY_CUDA(cudaEventRecord(ctx->ev[14], ctx->stream));
+        RSB_TRY_CUDA(cudaGraphLaunch(S->bexec, ctx->stream));
+        RSB_TRY_CUDA(cudaEventRecord(ctx->ev[15], ctx->stream));
+        RSB_TRY_CUDA(cudaEventSynchronize(ctx->ev[15]));
+        ctx->launches += S->graph_kernels;
+        float ms = 0.f;
+        RSB_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->ev[14], ctx->ev[15]));
+        it_total += ms;
+        for (int t = 0; t + 1 < S->btrace; t += 2) {
+            RSB_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->trace_ev[t], ctx->trace_ev[t + 1]));
+            tri_total += ms;
+        }
+    }
+    RSB_TRY(read_state(S));
+    *iter_ms = it_total;
+    *tri_ms = tri_total;
+    *tri_launches = k * (S->btrace / 2);
+    *kernels_per_iter = S->graph_kernels;
+    *status = S->h_st->status;
     return RSB_OK;
 }
 

@@ -7,6 +7,7 @@ bench.py uses them directly for device-resident timing.
 
 from __future__ import annotations
 
+import atexit
 import collections
 import ctypes
 import os
@@ -18,6 +19,20 @@ from . import _lib as L
 
 _ctx_lock = threading.Lock()
 _contexts: dict[int, "Context"] = {}
+_exiting = False
+
+
+@atexit.register
+def _at_exit():
+    # Interpreter teardown finalizes objects in no particular order; device
+    # handles are left to process exit (the driver reclaims the context)
+    # instead of being destroyed against an already-destroyed rsb_ctx.
+    global _exiting
+    _exiting = True
+
+
+def _alive(obj, attr="h"):
+    return not _exiting and getattr(obj, attr, None)
 
 
 def device_count() -> int:
@@ -70,7 +85,7 @@ class Context:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if _alive(self):
                 L.lib().rsb_ctx_destroy(self.h)
                 self.h = None
         except Exception:
@@ -110,7 +125,7 @@ class DeviceBuffer:
 
     def __del__(self):
         try:
-            if getattr(self, "ptr", None):
+            if _alive(self, "ptr"):
                 L.lib().rsb_device_free(self.ctx.h, self.ptr)
                 self.ptr = None
         except Exception:
@@ -129,7 +144,7 @@ class PinnedBuffer:
 
     def __del__(self):
         try:
-            if getattr(self, "ptr", None):
+            if _alive(self, "ptr"):
                 self.array = None
                 L.lib().rsb_host_free(self.ptr)
                 self.ptr = None
@@ -163,7 +178,7 @@ class DeviceMatrix:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if _alive(self):
                 L.lib().rsb_mat_destroy(self.h)
                 self.h = None
         except Exception:
@@ -260,7 +275,7 @@ class DevicePreconditioner:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if _alive(self):
                 L.lib().rsb_pre_destroy(self.h)
                 self.h = None
         except Exception:
@@ -319,7 +334,7 @@ class DeviceSolver:
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
+            if _alive(self):
                 L.lib().rsb_solver_destroy(self.h)
                 self.h = None
         except Exception:
