@@ -8,6 +8,7 @@
 // tasks by level and packs their entries in warp-interleaved slices (see
 // TriDev in rsb_internal.h) so the device solve reads them coalesced.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -149,7 +150,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         for (int64_t t = 0; t < n; ++t) order[pos[level[t]]++] = (int32_t)t;
     }
 
-    // warp-interleaved packing
+    // warp-interleaved packing: slice widths
     const int64_t nslices = (n + 31) / 32;
     std::vector<int64_t> soff(nslices + 1, 0);
     for (int64_t w = 0; w < nslices; ++w) {
@@ -161,20 +162,85 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         soff[w + 1] = soff[w] + 32 * K;
     }
     const int64_t slots = soff[nslices];
+
+    // variant: one CTA, level-synchronous, task data streamed into shared
+    // memory, for narrow DAGs whose chunks fit the shared-memory budget
+    const char *force = getenv("RSB_TRSV_VARIANT");  // "grid" | "cta" (experiments)
+    bool single_cta = n <= kCtaTriMaxN && (n / std::max<int64_t>(1, nlev)) <= kCtaTriMaxMeanWidth;
+    if (force && std::strcmp(force, "grid") == 0) single_cta = false;
+    if (force && std::strcmp(force, "cta") == 0 && n <= kCtaTriMaxN) single_cta = true;
+    int64_t ch = 0, emax = 0;
+    if (single_cta) {
+        for (int64_t cand : {1024, 512, 256, 128}) {
+            if (cand < maxw) break;
+            int64_t em = 0;
+            for (int64_t c0 = 0; c0 < nslices; c0 += cand / 32)
+                em = std::max(em, soff[std::min(nslices, c0 + cand / 32)] - soff[c0]);
+            em = std::max<int64_t>(32, em);
+            if (stage_smem_bytes(cand, em, !unit, nlev, (n + cand - 1) / cand) <= kStageSmemBudget) {
+                ch = cand;
+                emax = em;
+                break;
+            }
+        }
+        if (ch == 0) single_cta = false;
+    }
+    std::vector<int32_t> posof;
+    if (single_cta) {
+        posof.resize(n);
+        for (int64_t q = 0; q < n; ++q) posof[order[q]] = (int32_t)q;
+    }
+
     std::vector<int32_t> ecol(slots, -1);
     std::vector<double> eval(slots, 0.0);
+    const int64_t nchunks = single_cta ? (n + ch - 1) / ch : 0;
+    const int64_t padded = single_cta ? nchunks * ch : n;
     std::vector<double> tdiag;
-    if (!unit) tdiag.resize(n);
+    if (!unit) tdiag.assign(padded, 1.0);
+    std::vector<StageRec> recs;
+    std::vector<int32_t> tlen;
+    if (single_cta) {
+        recs.assign(slots, StageRec{0.0, -1, 0});
+        tlen.assign(padded, 0);
+    }
+    int64_t far = 0;
     for (int64_t w = 0; w < nslices; ++w) {
         for (int64_t l = 0; l < 32 && w * 32 + l < n; ++l) {
-            const int32_t t = order[w * 32 + l];
+            const int64_t q = w * 32 + l;  // task position
+            const int32_t t = order[q];
             for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
                 const int64_t e = soff[w] + (k - tptr[t]) * 32 + l;
-                ecol[e] = ent[k].col;
+                int32_t col = ent[k].col;
+                if (single_cta) {
+                    const int64_t p = posof[col];
+                    if (q - p + maxw < kRing) {
+                        recs[e] = StageRec{ent[k].val, (int32_t)((p & (kRing - 1)) * 8), 0};
+                        col = (int32_t)p;
+                    } else {
+                        recs[e] = StageRec{ent[k].val, -(col + 2), 0};
+                        col = -(col + 2);
+                        ++far;
+                    }
+                }
+                ecol[e] = col;
                 eval[e] = ent[k].val;
             }
-            if (!unit) tdiag[w * 32 + l] = diag[t];
+            if (single_cta) tlen[q] = (int32_t)(tptr[t + 1] - tptr[t]);
+            if (!unit) tdiag[q] = diag[t];
         }
+    }
+    std::vector<int32_t> rows(order.begin(), order.end());
+    rows.resize(padded, 0);
+    std::vector<int64_t> ceoff;
+    std::vector<int32_t> sl;
+    const int64_t slw = ch / 32 + 4;
+    if (single_cta) {
+        ceoff.resize(nchunks + 1);
+        sl.assign(nchunks * slw, 0);
+        for (int64_t c = 0; c <= nchunks; ++c) ceoff[c] = soff[std::min(nslices, c * (ch / 32))];
+        for (int64_t c = 0; c < nchunks; ++c)
+            for (int64_t wl = 0; wl <= ch / 32; ++wl)
+                sl[c * slw + wl] = (int32_t)(soff[std::min(nslices, c * (ch / 32) + wl)] - ceoff[c]);
     }
 
     rsb_ctx *ctx = T->ctx;
@@ -185,12 +251,31 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     S->max_width = maxw;
     S->entries = slots;
     S->mode = (is_dot ? 1 : 0) | (unit ? 0 : 2);
+    S->single_cta = single_cta;
+    S->far_entries = far;
+    S->has_far = far > 0;
+    S->stage_ch = (int32_t)ch;
+    S->stage_emax = (int32_t)emax;
+    S->nchunks = (int32_t)nchunks;
+    S->padded_n = padded;
+    if (const char *ex = getenv("RSB_TRSV_EXPERIMENT")) S->experiment = atoi(ex);
     int rc = RSB_OK;
-    if ((rc = dev_upload(ctx, &S->task_row, order.data(), n)) != RSB_OK ||
+    if (S->single_cta && (rc = prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
+        delete S;
+        return rc;
+    }
+    std::vector<int32_t> lptr(lstart.begin(), lstart.end());
+    if ((rc = dev_upload(ctx, &S->level_ptr, lptr.data(), lptr.size())) != RSB_OK ||
+        (rc = dev_upload(ctx, &S->task_row, rows.data(), rows.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->slice_off, soff.data(), nslices + 1)) != RSB_OK ||
         (rc = dev_upload(ctx, &S->ecol, ecol.data(), slots)) != RSB_OK ||
         (rc = dev_upload(ctx, &S->eval, eval.data(), slots)) != RSB_OK ||
-        (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), n)) != RSB_OK) ||
+        (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), tdiag.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->chunk_eoff, ceoff.data(), ceoff.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->sloc, sl.data(), sl.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_alloc(ctx, (void **)&S->bpos, padded * sizeof(double))) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->tlen, tlen.data(), tlen.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK) {
         tri_free(ctx, S);
         return rc;
@@ -208,13 +293,19 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
 
 void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (!s) return;
-    const int64_t n = s->n, nslices = (n + 31) / 32;
-    dev_free(ctx, s->task_row, n * sizeof(int32_t));
+    const int64_t n = s->n, nslices = (n + 31) / 32, padded = s->padded_n ? s->padded_n : n;
+    dev_free(ctx, s->task_row, padded * sizeof(int32_t));
     dev_free(ctx, s->slice_off, (nslices + 1) * sizeof(int64_t));
     dev_free(ctx, s->ecol, s->entries * sizeof(int32_t));
     dev_free(ctx, s->eval, s->entries * sizeof(double));
-    if (s->diag) dev_free(ctx, s->diag, n * sizeof(double));
+    if (s->diag) dev_free(ctx, s->diag, padded * sizeof(double));
+    if (s->chunk_eoff) dev_free(ctx, s->chunk_eoff, (s->nchunks + 1) * sizeof(int64_t));
+    if (s->sloc) dev_free(ctx, s->sloc, (size_t)s->nchunks * (s->stage_ch / 32 + 4) * sizeof(int32_t));
+    if (s->bpos) dev_free(ctx, s->bpos, padded * sizeof(double));
+    if (s->recs) dev_free(ctx, s->recs, s->entries * sizeof(StageRec));
+    if (s->tlen) dev_free(ctx, s->tlen, padded * sizeof(int32_t));
     dev_free(ctx, s->ticket, sizeof(unsigned long long));
+    dev_free(ctx, s->level_ptr, (s->nlevels + 1) * sizeof(int32_t));
     delete s;
 }
 

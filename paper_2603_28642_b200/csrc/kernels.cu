@@ -6,6 +6,8 @@
 // -fmad=false: a*b+c is two roundings unless fma() is written out.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "rsb_internal.h"
 
 namespace rsb {
@@ -14,6 +16,8 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kTriBlock = 128;
+constexpr int kCtaTri = 128;
+constexpr int kStageRegs = 16;  // entries per task held in registers by the staged solve
 
 __device__ __forceinline__ bool gated(const Gate &g) {
     return (g.a && *(volatile const int *)g.a) || (g.b && *(volatile const int *)g.b);
@@ -211,7 +215,8 @@ __device__ __forceinline__ void publish(double *p, double v) {
 }
 
 // blas-order dot of a task's gathered entries, one thread (len >= 16 path)
-__device__ double task_blas_dot(const TriDev &T, int64_t base, int lane, int len, const double *x) {
+template <class Wait>
+__device__ double task_blas_dot(const TriDev &T, int64_t base, int lane, int len, Wait wait) {
     auto ent = [&](int k) { return base + (int64_t)k * 32 + lane; };
     const int n1 = len & ~15, n32 = n1 & ~31;
     double dot = 0.0;
@@ -220,22 +225,128 @@ __device__ double task_blas_dot(const TriDev &T, int64_t base, int lane, int len
         for (int q = 0; q < 32; ++q) a5[q] = 0.0;
         int i = 0;
         for (; i < n32; i += 32)
-            for (int q = 0; q < 32; ++q)
-                a5[q] = fma(T.eval[ent(i + q)], wait_ready(x + T.ecol[ent(i + q)]), a5[q]);
+            for (int q = 0; q < 32; ++q) a5[q] = fma(T.eval[ent(i + q)], wait(T.ecol[ent(i + q)]), a5[q]);
         double a[16];
         for (int gq = 0; gq < 4; ++gq)
             for (int k = 0; k < 4; ++k) a[4 * gq + k] = a5[8 * gq + k] + a5[8 * gq + k + 4];
         for (; i < n1; i += 16)
-            for (int q = 0; q < 16; ++q)
-                a[q] = fma(T.eval[ent(i + q)], wait_ready(x + T.ecol[ent(i + q)]), a[q]);
+            for (int q = 0; q < 16; ++q) a[q] = fma(T.eval[ent(i + q)], wait(T.ecol[ent(i + q)]), a[q]);
         double t[4];
         for (int k = 0; k < 4; ++k) t[k] = ((a[k] + a[4 + k]) + a[8 + k]) + a[12 + k];
         dot = (t[0] + t[2]) + (t[1] + t[3]);
     }
-    for (int k = n1; k < len; ++k) dot = fma(wait_ready(x + T.ecol[ent(k)]), T.eval[ent(k)], dot);
+    for (int k = n1; k < len; ++k) dot = fma(wait(T.ecol[ent(k)]), T.eval[ent(k)], dot);
     return dot;
 }
 
+// One task's loads that do not depend on other unknowns (its first kPre
+// entries, the right-hand side, the diagonal), issued before any wait.
+constexpr int kPre = 12;
+
+struct Task {
+    int t, row, lane, K, len;  // len: number of real entries (K is the slice's padded width)
+    int64_t base;
+    int cols[kPre];
+    double vals[kPre];
+    double acc;  // right-hand side
+    double d;    // diagonal (divide) or 1
+};
+
+template <int MODE>
+__device__ __forceinline__ void load_task(const TriDev &T, int t, const VecIn &a, const double *c, Task &k) {
+    k.t = t;
+    k.lane = t & 31;
+    k.row = T.task_row[t];
+    const int w = t >> 5;
+    k.base = T.slice_off[w];
+    k.K = (int)((T.slice_off[w + 1] - k.base) >> 5);
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+        k.cols[q] = -1;
+        k.vals[q] = 0.0;
+        if (q < k.K) {
+            k.cols[q] = T.ecol[k.base + (int64_t)q * 32 + k.lane];
+            k.vals[q] = T.eval[k.base + (int64_t)q * 32 + k.lane];
+        }
+    }
+    double acc = vin(a, k.row);
+    if (c) acc = __dadd_rn(acc, c[k.row]);
+    k.acc = acc;
+    k.d = (MODE & 2) ? T.diag[t] : 1.0;
+    int len = 0;
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) len += k.cols[q] >= 0;
+    if (len == kPre)
+        while (len < k.K && T.ecol[k.base + (int64_t)len * 32 + k.lane] >= 0) ++len;
+    k.len = len;
+}
+
+// true when every dependency of the task is finished (never blocks)
+template <class Ready>
+__device__ __forceinline__ bool task_ready(const TriDev &T, const Task &k, Ready ready) {
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < kPre; ++q)
+        if (k.cols[q] >= 0) ok &= ready(k.cols[q]);
+    if (ok && k.len > kPre)
+        for (int q = kPre; q < k.len; ++q) {
+            if (!ready(T.ecol[k.base + (int64_t)q * 32 + k.lane])) return false;
+        }
+    return ok;
+}
+
+// The task's value, all dependencies finished; read(j) returns x_j.
+// Sequential mode (sc.py:253-262, 271-278): acc -= l_ij * x_j in stored order,
+// skipping x_j == 0.  Dot mode (sc.py:291,296,311): acc -= OpenBLAS ddot of
+// the gathered values.  Then acc /= d for a stored diagonal.
+template <int MODE, class Read>
+__device__ __forceinline__ double task_value(const TriDev &T, const Task &k, Read read) {
+    double acc = k.acc;
+    if (!(MODE & 1)) {
+#pragma unroll
+        for (int q = 0; q < kPre; ++q) {
+            if (q < k.len) {
+                const double xj = read(k.cols[q]);
+                if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(k.vals[q], xj));
+            }
+        }
+        for (int q = kPre; q < k.len; ++q) {
+            const int64_t e = k.base + (int64_t)q * 32 + k.lane;
+            const double xj = read(T.ecol[e]);
+            if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(T.eval[e], xj));
+        }
+    } else if (k.len > 0) {
+        double dot = 0.0;
+        if (k.len <= kPre) {
+#pragma unroll
+            for (int q = 0; q < kPre; ++q)
+                if (q < k.len) dot = fma(k.vals[q], read(k.cols[q]), dot);
+        } else if (k.len < 16) {
+            for (int q = 0; q < k.len; ++q) {
+                const int64_t e = k.base + (int64_t)q * 32 + k.lane;
+                dot = fma(T.eval[e], read(T.ecol[e]), dot);
+            }
+        } else {
+            dot = task_blas_dot(T, k.base, k.lane, k.len, read);
+        }
+        acc = __dsub_rn(acc, dot);
+    }
+    if (MODE & 2) acc = __ddiv_rn(acc, k.d);
+    return acc;
+}
+
+__device__ __forceinline__ double ld_relaxed(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double(v);
+}
+
+// Grid-wide variant (wide DAGs): completion = the output entry is no longer
+// the sentinel, observed through L2 with relaxed gpu-scope loads.  Blocks take
+// consecutive task ranges in the order they start (atomic ticket), so a task
+// only waits on blocks already resident or done.  Warp-synchronous polling:
+// lanes never spin divergently; every round each pending lane checks all its
+// dependencies, the ready ones compute and publish, and the warp reconverges.
 template <int MODE>
 __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const double *c, double *x,
                                                     Gate g) {
@@ -244,40 +355,225 @@ __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const dou
     if (threadIdx.x == 0) s_blk = (int)(atomicAdd(T.ticket, 1ull) % gridDim.x);
     __syncthreads();
     const int t = s_blk * kTriBlock + threadIdx.x;
-    if (t >= T.n) return;
-    const int row = T.task_row[t];
-    double acc = vin(a, row);
-    if (c) acc = __dadd_rn(acc, c[row]);
-    const int w = t >> 5, lane = t & 31;
-    const int64_t base = T.slice_off[w];
-    const int K = (int)((T.slice_off[w + 1] - base) >> 5);
-    if (!(MODE & 1)) {
-        for (int k = 0; k < K; ++k) {
-            const int j = T.ecol[base + (int64_t)k * 32 + lane];
-            if (j < 0) break;
-            const double v = T.eval[base + (int64_t)k * 32 + lane];
-            const double xj = wait_ready(x + j);
-            if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(v, xj));
+    bool pending = t < T.n;
+    Task k;
+    if (pending) load_task<MODE>(T, t, a, c, k);
+    auto ready = [&](int j) { return __double_as_longlong(ld_relaxed(x + j)) != (long long)kSentinel; };
+    while (__any_sync(0xffffffffu, pending)) {
+        if (pending && task_ready(T, k, ready)) {
+            publish(x + k.row, task_value<MODE>(T, k, [&](int j) { return ld_relaxed(x + j); }));
+            pending = false;
         }
-    } else {
-        int len = 0;
-        while (len < K && T.ecol[base + (int64_t)len * 32 + lane] >= 0) ++len;
-        if (len > 0) {
-            double dot;
-            if (len < 16) {
-                dot = 0.0;
-                for (int k = 0; k < len; ++k) {
-                    const int64_t e = base + (int64_t)k * 32 + lane;
-                    dot = fma(T.eval[e], wait_ready(x + T.ecol[e]), dot);
-                }
-            } else {
-                dot = task_blas_dot(T, base, lane, len, x);
-            }
-            acc = __dsub_rn(acc, dot);
-        }
+        __syncwarp();
     }
-    if (MODE & 2) acc = __ddiv_rn(acc, T.diag[t]);
-    publish(x + row, acc);
+}
+
+__device__ __forceinline__ double canonical(double v) {
+    return __double_as_longlong(v) == (long long)kSentinel ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
+
+// ---- shared-memory staging primitives (sm_90+: mbarrier + 1-D TMA bulk copy)
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// right-hand side in task-position order: bpos[t] = a(row_t) [+ c[row_t]]
+__global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row, VecIn a, const double *c,
+                             double *bpos, Gate g) {
+    if (gated(g)) return;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < padded; t += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (t < n) {
+            const int row = task_row[t];
+            v = vin(a, row);
+            if (c) v = __dadd_rn(v, c[row]);
+        }
+        bpos[t] = v;
+    }
+}
+
+// Single-CTA level-synchronous solve with shared-memory staging (narrow DAGs,
+// e.g. config 1 at mu = 1: 1,290 / 2,806 levels of <= 66 unknowns).
+//
+// The dependency chain crosses one barrier per level and touches only
+// shared memory:
+//   - task data of positions [c*CH, (c+1)*CH) -- gathered right-hand sides,
+//     diagonals, 16-byte entry records {value, source}, rows, lengths -- is
+//     streamed into one of kStageBufs shared-memory buffers by 1-D TMA bulk
+//     copies completing on an mbarrier, issued kStageBufs-1 chunks ahead;
+//   - solved values go to a shared-memory ring indexed by task position; an
+//     entry's source is the byte offset of its ring slot when the slot is
+//     still live (distance + widest level < kRing), else -(row + 2) and the
+//     value is read from the global output (FAR specialisation only);
+//   - a task issues all its entry and ring loads before the ordered FP chain.
+// Earlier designs measured 0.9-3 us per level (grid-wide sync-free, CTA
+// spin-polling: spinning warps starved the critical warp of issue slots;
+// per-thread prefetch: dependent global loads in front of every barrier);
+// see profiles/.
+// x[rows] @ vals in OpenBLAS association for a staged task with >= 16 entries
+// (rare: L^T columns hold at most p entries); out of line to keep the fast
+// path's registers free.
+__device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const unsigned char *ring,
+                                            const double *x, bool far) {
+    auto la = [&](int q) { return rec[q * 32].v; };
+    auto lb = [&](int q) {
+        const int s = rec[q * 32].src;
+        return (!far || s >= 0) ? *reinterpret_cast<const double *>(ring + s) : x[-s - 2];
+    };
+    const int n1 = len & ~15, n32 = n1 & ~31;
+    double dot = 0.0;
+    if (n1) {
+        double a5[32];
+        for (int q = 0; q < 32; ++q) a5[q] = 0.0;
+        int i = 0;
+        for (; i < n32; i += 32)
+            for (int q = 0; q < 32; ++q) a5[q] = fma(la(i + q), lb(i + q), a5[q]);
+        double a4[16];
+        for (int gq = 0; gq < 4; ++gq)
+            for (int kk = 0; kk < 4; ++kk) a4[4 * gq + kk] = a5[8 * gq + kk] + a5[8 * gq + kk + 4];
+        for (; i < n1; i += 16)
+            for (int q = 0; q < 16; ++q) a4[q] = fma(la(i + q), lb(i + q), a4[q]);
+        double tt[4];
+        for (int kk = 0; kk < 4; ++kk) tt[kk] = ((a4[kk] + a4[4 + kk]) + a4[8 + kk]) + a4[12 + kk];
+        dot = (tt[0] + tt[2]) + (tt[1] + tt[3]);
+    }
+    for (int q = n1; q < len; ++q) dot = fma(lb(q), la(q), dot);
+    return dot;
+}
+
+template <int MODE, bool FAR>
+__global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gate g) {
+    if (gated(g)) return;
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr bool kDiag = (MODE & 2) != 0;
+    const int CH = T.stage_ch, EM = T.stage_emax, SLW = CH / 32 + 4;
+    unsigned char *ring = smem;
+    unsigned char *bufs = smem + (size_t)kRing * 8;
+    const size_t o_d = (size_t)CH * 8, o_rec = o_d + (kDiag ? (size_t)CH * 8 : 0), o_row = o_rec + (size_t)EM * 16,
+                 o_len = o_row + (size_t)CH * 4, o_sl = o_len + (size_t)CH * 4, bb = o_sl + (size_t)SLW * 4;
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * bb);
+    int *lvl = reinterpret_cast<int *>(mbar + 2 * kStageBufs);
+    const int nlev = T.nlevels, nch = T.nchunks, lgch = __ffs(CH) - 1;
+    // per-chunk entry counts (the issuing thread must not wait on global loads)
+    int *cne = lvl + ((nlev + 4) & ~3);
+    for (int i = threadIdx.x; i <= nlev; i += blockDim.x) lvl[i] = T.level_ptr[i];
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) cne[c] = (int)(T.chunk_eoff[c + 1] - T.chunk_eoff[c]);
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kStageBufs; ++b) mbar_init(&mbar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    long long e_next = 0;  // entry offset of the next chunk to issue (thread 0)
+    auto issue = [&](int c) {  // thread 0 only
+        unsigned char *B = bufs + (size_t)(c & (kStageBufs - 1)) * bb;
+        const int64_t e0 = e_next, ne = cne[c];
+        e_next += ne;
+        const unsigned bytes = (unsigned)(CH * 8 + (kDiag ? CH * 8 : 0) + ne * 16 + CH * 8 + SLW * 4);
+        unsigned long long *bar = &mbar[c & (kStageBufs - 1)];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(B, T.bpos + (int64_t)c * CH, CH * 8, bar);
+        if (kDiag) bulk_g2s(B + o_d, T.diag + (int64_t)c * CH, CH * 8, bar);
+        if (ne) bulk_g2s(B + o_rec, T.recs + e0, (unsigned)(ne * 16), bar);
+        bulk_g2s(B + o_row, T.task_row + (int64_t)c * CH, CH * 4, bar);
+        bulk_g2s(B + o_len, T.tlen + (int64_t)c * CH, CH * 4, bar);
+        bulk_g2s(B + o_sl, T.sloc + (int64_t)c * SLW, SLW * 4, bar);
+    };
+    int issued = min(kStageBufs, nch), ready = -1;
+    if (threadIdx.x == 0)
+        for (int c = 0; c < issued; ++c) issue(c);
+    auto src = [&](int s) -> double {
+        if (!FAR || s >= 0) return *reinterpret_cast<const double *>(ring + s);
+        return x[-s - 2];
+    };
+    for (int l = 0; l < nlev; ++l) {
+        const int lo = lvl[l], hi = lvl[l + 1];
+        const int first = lo >> lgch;  // refill buffers whose chunk lies wholly before this level
+        while (issued < nch && issued < first + kStageBufs) {
+            if (threadIdx.x == 0) issue(issued);
+            ++issued;
+        }
+        const int last = (hi - 1) >> lgch;  // chunks this level reads must have landed
+        while (ready < last) {
+            ++ready;
+            mbar_wait(&mbar[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
+        }
+        for (int t = lo + threadIdx.x; t < hi; t += kCtaTri) {
+            const int loc = t & (CH - 1);
+            const unsigned char *B = bufs + (size_t)((t >> lgch) & (kStageBufs - 1)) * bb;
+            const int len = reinterpret_cast<const int *>(B + o_len)[loc];
+            const int row = reinterpret_cast<const int *>(B + o_row)[loc];
+            const StageRec *rec = reinterpret_cast<const StageRec *>(B + o_rec) +
+                                  reinterpret_cast<const int *>(B + o_sl)[loc >> 5] + (t & 31);
+            double acc = reinterpret_cast<const double *>(B)[loc];
+            const double d = kDiag ? reinterpret_cast<const double *>(B + o_d)[loc] : 1.0;
+            double vv[kStageRegs], xv[kStageRegs];
+#pragma unroll
+            for (int q = 0; q < kStageRegs; ++q) {
+                if (q < len) {
+                    const StageRec r = rec[q * 32];
+                    vv[q] = r.v;
+                    xv[q] = src(r.src);
+                }
+            }
+            if (!(MODE & 1)) {
+                // x_i -= l_ij * x_j in stored order, skipped when x_j == 0 (sc.py:261-262)
+#pragma unroll
+                for (int q = 0; q < kStageRegs; ++q) {
+                    if (q >= len) break;
+                    if (xv[q] != 0.0) acc = __dsub_rn(acc, __dmul_rn(vv[q], xv[q]));
+                }
+                for (int q = kStageRegs; q < len; ++q) {
+                    const StageRec r = rec[q * 32];
+                    const double xj = src(r.src);
+                    if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(r.v, xj));
+                }
+            } else if (len > 0) {
+                // x_j -= vals @ x[rows]: OpenBLAS ddot order (sc.py:291,296,311)
+                double dot = 0.0;
+                if (len < 16) {
+#pragma unroll
+                    for (int q = 0; q < kStageRegs; ++q) {
+                        if (q >= len) break;
+                        dot = fma(vv[q], xv[q], dot);
+                    }
+                    for (int q = kStageRegs; q < len; ++q) {
+                        const StageRec r = rec[q * 32];
+                        dot = fma(r.v, src(r.src), dot);
+                    }
+                } else {
+                    dot = rec_blas_dot(rec, len, ring, x, FAR);
+                }
+                acc = __dsub_rn(acc, dot);
+            }
+            if (kDiag) acc = __ddiv_rn(acc, d);
+            const double v = canonical(acc);
+            *reinterpret_cast<double *>(ring + (size_t)(t & (kRing - 1)) * 8) = v;
+            x[row] = v;
+        }
+        __syncthreads();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -420,18 +716,53 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
     const bool trace = ctx->tracing && ctx->trace_n + 2 <= 64;
     if (trace)
         RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
-    RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
-    const int grid = grid_for(T.n, kTriBlock);
     const TriDev v = T.view();
-    switch (T.mode) {
-        case 0: k_trsv<0><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
-        case 1: k_trsv<1><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
-        case 2: k_trsv<2><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
-        default: k_trsv<3><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+    if (T.single_cta) {
+        const size_t smem = (size_t)stage_smem_bytes(T.stage_ch, T.stage_emax, T.diag != nullptr, T.nlevels, T.nchunks);
+        k_gather_pos<<<grid_stride(T.padded_n), kBlock, 0, ctx->stream>>>(T.n, T.padded_n, T.task_row, a, c,
+                                                                          T.bpos, g);
+        RSB_TRY(post_launch(ctx));
+        const int sel = T.mode + (T.has_far ? 4 : 0);
+        switch (sel) {
+            case 0: k_trsv_stage<0, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 1: k_trsv_stage<1, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 2: k_trsv_stage<2, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 3: k_trsv_stage<3, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 4: k_trsv_stage<0, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 5: k_trsv_stage<1, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 6: k_trsv_stage<2, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            default: k_trsv_stage<3, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+        }
+    } else {
+        RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
+        const int grid = grid_for(T.n, kTriBlock);
+        switch (T.mode) {
+            case 0: k_trsv<0><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+            case 1: k_trsv<1><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+            case 2: k_trsv<2><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+            default: k_trsv<3><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
+        }
     }
     RSB_TRY(post_launch(ctx));
     if (trace)
         RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
+    return RSB_OK;
+}
+
+int prepare_trsv_cta(int64_t smem_bytes) {
+    static int granted = 48 * 1024;  // attributes only ever grow: every schedule keeps its launch valid
+    const int smem = (int)smem_bytes;
+    if (smem > granted) {
+        granted = smem;
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        RSB_TRY_CUDA(cudaFuncSetAttribute(k_trsv_stage<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     return RSB_OK;
 }
 

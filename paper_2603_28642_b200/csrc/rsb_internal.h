@@ -37,6 +37,38 @@ void set_error(const char *fmt, ...);
 // bits, so no finished entry can look unfinished.
 constexpr unsigned long long kSentinel = 0xFFF4D15EA5E0C0DEull;
 
+// Largest order solved by the single-CTA triangular kernel (one byte of
+// shared memory per unknown) and the mean level width below which it is
+// chosen over the grid-wide kernel.
+constexpr int64_t kCtaTriMaxN = 1 << 20;
+constexpr int64_t kCtaTriMaxMeanWidth = 4096;
+// Single-CTA solve: values of recently solved tasks live in a shared-memory
+// ring indexed by task position (kRing slots).  With one barrier per level, a
+// slot written at position p is reused by position p + kRing, so a dependency
+// at distance d is still live if d + (widest level) < kRing.
+constexpr int kRing = 4096;
+constexpr int kStageBufs = 4;
+constexpr int kStageSmemBudget = 220 * 1024;
+// shared-memory bytes of one staging buffer
+inline int64_t stage_buf_bytes(int64_t ch, int64_t emax, bool diag) {
+    // rhs, [diag], entry records (16 B), rows, lengths, slice offsets
+    return ch * 8 + (diag ? ch * 8 : 0) + emax * 16 + ch * 4 + ch * 4 + (ch / 32 + 4) * 4;
+}
+
+// One entry of a staged solve: the factor value and where its unknown is read
+// from -- the byte offset of its ring slot (>= 0), or -(row + 2) for a
+// dependency older than the ring.
+struct alignas(16) StageRec {
+    double v;
+    int32_t src;
+    int32_t pad;
+};
+inline int64_t stage_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels, int64_t nchunks) {
+    // ring, staging buffers, mbarriers, level bounds (padded to 4), chunk entry counts
+    return (int64_t)kRing * 8 + kStageBufs * stage_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
+           ((nlevels + 4) & ~3LL) * 4 + nchunks * 4;
+}
+
 // ---------------------------------------------------------------------------
 // device-side views (passed by value to kernels)
 // ---------------------------------------------------------------------------
@@ -83,6 +115,23 @@ struct TriDev {
     const double *eval;
     const double *diag;  // per task, nullptr when unit
     unsigned long long *ticket;
+    // single-CTA schedules: ecol holds the dependency's task position when
+    // its ring slot is still live (>= 0), else -(row + 2); tasks of level l
+    // are positions level_ptr[l] .. level_ptr[l+1]
+    int32_t has_far;
+    int32_t nlevels;
+    const int32_t *level_ptr;
+    // staged single-CTA solve: task data is streamed into shared memory in
+    // chunks of stage_ch positions (TMA bulk copies, kStageBufs deep)
+    int32_t stage_ch;     // positions per chunk (multiple of 128, >= widest level)
+    int32_t stage_emax;   // max entry slots of a chunk
+    int32_t nchunks;
+    const int64_t *chunk_eoff;  // entry-slot offset of each chunk (nchunks + 1)
+    const int32_t *sloc;        // per chunk: slice offsets local to the chunk (stage_ch/32 + 4)
+    double *bpos;               // right-hand side gathered into position order
+    int32_t experiment;         // timing experiments only (RSB_TRSV_EXPERIMENT)
+    const StageRec *recs;       // entry records in the warp-interleaved slot order
+    const int32_t *tlen;        // entries per task (position order, padded)
 };
 
 // ---------------------------------------------------------------------------
@@ -109,8 +158,22 @@ struct TriSched {
     double *diag = nullptr;
     unsigned long long *ticket = nullptr;
     int32_t mode = 0;
+    bool single_cta = false;  // run on one CTA with a shared-memory value ring (narrow DAG)
+    int32_t has_far = 0;
+    int64_t far_entries = 0;
+    int32_t *level_ptr = nullptr;  // nlevels + 1 task positions
+    int32_t stage_ch = 0, stage_emax = 0, nchunks = 0;
+    int64_t *chunk_eoff = nullptr;
+    int32_t *sloc = nullptr;
+    double *bpos = nullptr;
+    int64_t padded_n = 0;  // task_row / diag / bpos lengths (nchunks * stage_ch when staged)
+    int32_t experiment = 0;
+    StageRec *recs = nullptr;
+    int32_t *tlen = nullptr;
     TriDev view() const {
-        return TriDev{n, mode, task_row, slice_off, ecol, eval, diag, ticket};
+        return TriDev{n,        mode,       task_row, slice_off,  ecol, eval, diag,       ticket,
+                      has_far,  (int32_t)nlevels,      level_ptr, stage_ch, stage_emax, nchunks,
+                      chunk_eoff, sloc,     bpos,     experiment, recs, tlen};
     }
 };
 
@@ -185,6 +248,8 @@ int stage_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s);
 int finish_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s);
 // cached level-ordered schedule of (matrix, kind)
 int get_tri(rsb_mat *T, int kind, TriSched **out);
+// one-time kernel attribute setup for the single-CTA triangular solve of order n
+int prepare_trsv_cta(int64_t n);
 // one-time kernel attribute setup for the dense S solve of size s
 int prepare_chol(int64_t s);
 

@@ -1,0 +1,23 @@
+"""Per-phase cycle breakdown of the staged single-CTA triangular solve, thread 0
+(experiment mode 3: the kernel writes clock64 totals into x[0..4])."""
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["RSB_TRSV_EXPERIMENT"] = "3"
+import paper_2603_28642_b200 as P
+from paper_2603_28642_b200 import _lib as L
+from paper_2603_28642_b200 import workloads as W
+from paper_2603_28642_b200.device import DeviceBuffer, DeviceMatrix, get_context
+A, _ = W.config1(seed=1, g=256)
+S, _ = P.column_scale(A)
+f = P.ilup_factorize(S, P.IlupParams(p=10, tau=0.0, mu=1.0))
+ctx = get_context(); n = f.U.ncols
+b = DeviceBuffer(ctx, n); b.upload(np.random.default_rng(0).standard_normal(n)); x = DeviceBuffer(ctx, n)
+out = {}
+for name, M, kind in (("L1", f.L1, L.TRI_LOWER_UNIT), ("L1T", f.L1, L.TRI_LOWER_T_UNIT), ("U", f.U, L.TRI_UPPER)):
+    dm = DeviceMatrix(M, ctx)
+    for _ in range(3):
+        L.check(L.lib().rsb_trsv(dm.h, kind, b.ptr, x.ptr, L.RSB_DEVICE))
+    v = x.download()[:5]
+    out[name] = {k: round(v[i] / v[4], 1) for i, k in enumerate(["issue", "wait", "task", "barrier"])}
+print(json.dumps(out))
