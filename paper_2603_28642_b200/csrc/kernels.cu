@@ -528,9 +528,13 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
                                   reinterpret_cast<const int *>(B + o_sl)[loc >> 5] + (t & 31);
             double acc = reinterpret_cast<const double *>(B)[loc];
             const double d = kDiag ? reinterpret_cast<const double *>(B + o_d)[loc] : 1.0;
+            // warp-uniform trip count: the longest task among the active lanes
+            const int wlen = __reduce_max_sync(__activemask(), len);
             double vv[kStageRegs], xv[kStageRegs];
 #pragma unroll
             for (int q = 0; q < kStageRegs; ++q) {
+                vv[q] = 0.0;
+                xv[q] = 0.0;
                 if (q < len) {
                     const StageRec r = rec[q * 32];
                     vv[q] = r.v;
@@ -541,8 +545,10 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
                 // x_i -= l_ij * x_j in stored order, skipped when x_j == 0 (sc.py:261-262)
 #pragma unroll
                 for (int q = 0; q < kStageRegs; ++q) {
-                    if (q >= len) break;
-                    if (xv[q] != 0.0) acc = __dsub_rn(acc, __dmul_rn(vv[q], xv[q]));
+                    if (q >= wlen) break;  // uniform across the warp
+                    // predicated, not branched: lanes have different lengths
+                    const double nx = __dsub_rn(acc, __dmul_rn(vv[q], xv[q]));
+                    acc = (q < len && xv[q] != 0.0) ? nx : acc;
                 }
                 for (int q = kStageRegs; q < len; ++q) {
                     const StageRec r = rec[q * 32];
@@ -555,8 +561,9 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
                 if (len < 16) {
 #pragma unroll
                     for (int q = 0; q < kStageRegs; ++q) {
-                        if (q >= len) break;
-                        dot = fma(vv[q], xv[q], dot);
+                        if (q >= wlen) break;  // uniform across the warp
+                        const double nd = fma(vv[q], xv[q], dot);
+                        dot = q < len ? nd : dot;
                     }
                     for (int q = kStageRegs; q < len; ++q) {
                         const StageRec r = rec[q * 32];
