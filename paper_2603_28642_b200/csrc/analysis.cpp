@@ -169,14 +169,17 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     bool single_cta = n <= kCtaTriMaxN && (n / std::max<int64_t>(1, nlev)) <= kCtaTriMaxMeanWidth;
     if (force && std::strcmp(force, "grid") == 0) single_cta = false;
     if (force && std::strcmp(force, "cta") == 0 && n <= kCtaTriMaxN) single_cta = true;
+    // records per position (contiguous per task) and their prefix sums
+    std::vector<int64_t> rpre;
     int64_t ch = 0, emax = 0;
     if (single_cta) {
+        rpre.assign(n + 1, 0);
+        for (int64_t q = 0; q < n; ++q) rpre[q + 1] = rpre[q] + (tptr[order[q] + 1] - tptr[order[q]]);
         for (int64_t cand : {1024, 512, 256, 128}) {
             if (cand < maxw) break;
             int64_t em = 0;
-            for (int64_t c0 = 0; c0 < nslices; c0 += cand / 32)
-                em = std::max(em, soff[std::min(nslices, c0 + cand / 32)] - soff[c0]);
-            em = std::max<int64_t>(32, em);
+            for (int64_t c0 = 0; c0 < n; c0 += cand) em = std::max(em, rpre[std::min(n, c0 + cand)] - rpre[c0]);
+            em = std::max<int64_t>(2, (em + 1) & ~1LL);
             if (stage_smem_bytes(cand, em, !unit, nlev, (n + cand - 1) / cand) <= kStageSmemBudget) {
                 ch = cand;
                 emax = em;
@@ -197,51 +200,57 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     const int64_t padded = single_cta ? nchunks * ch : n;
     std::vector<double> tdiag;
     if (!unit) tdiag.assign(padded, 1.0);
-    std::vector<StageRec> recs;
-    std::vector<int32_t> tlen;
-    if (single_cta) {
-        recs.assign(slots, StageRec{0.0, -1, 0});
-        tlen.assign(padded, 0);
-    }
-    int64_t far = 0;
     for (int64_t w = 0; w < nslices; ++w) {
         for (int64_t l = 0; l < 32 && w * 32 + l < n; ++l) {
             const int64_t q = w * 32 + l;  // task position
             const int32_t t = order[q];
             for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
                 const int64_t e = soff[w] + (k - tptr[t]) * 32 + l;
-                int32_t col = ent[k].col;
-                if (single_cta) {
-                    const int64_t p = posof[col];
-                    if (q - p + maxw < kRing) {
-                        recs[e] = StageRec{ent[k].val, (int32_t)((p & (kRing - 1)) * 8), 0};
-                        col = (int32_t)p;
-                    } else {
-                        recs[e] = StageRec{ent[k].val, -(col + 2), 0};
-                        col = -(col + 2);
-                        ++far;
-                    }
-                }
-                ecol[e] = col;
+                ecol[e] = ent[k].col;
                 eval[e] = ent[k].val;
             }
-            if (single_cta) tlen[q] = (int32_t)(tptr[t + 1] - tptr[t]);
             if (!unit) tdiag[q] = diag[t];
+        }
+    }
+    // staged layout: per-position meta, {diag, 1/diag}, contiguous records whose
+    // source is the ring byte offset of a live dependency or -(row + 2)
+    std::vector<StageRec> recs;
+    std::vector<StageMeta> meta;
+    std::vector<double> dd;
+    std::vector<int64_t> croff;
+    int64_t far = 0;
+    if (single_cta) {
+        recs.resize(std::max<int64_t>(2, rpre[n]));
+        meta.assign(padded, StageMeta{0, 0, 0, 0});
+        croff.resize(nchunks + 1);
+        for (int64_t c = 0; c <= nchunks; ++c) croff[c] = rpre[std::min(n, c * ch)];
+        for (int64_t q = 0; q < n; ++q) {
+            const int32_t t = order[q];
+            const int64_t r0 = rpre[q];
+            for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
+                const int32_t col = ent[k].col;
+                const int64_t p = posof[col];
+                int32_t src;
+                if (q - p + maxw < kRing) {
+                    src = (int32_t)((p & (kRing - 1)) * 8);
+                } else {
+                    src = -(col + 2);
+                    ++far;
+                }
+                recs[r0 + (k - tptr[t])] = StageRec{ent[k].val, src, 0};
+            }
+            meta[q] = StageMeta{t, (int32_t)(tptr[t + 1] - tptr[t]), (int32_t)(r0 - croff[q / ch]), 0};
+        }
+        if (!unit) {
+            dd.assign(2 * padded, 1.0);
+            for (int64_t q = 0; q < padded; ++q) {
+                dd[2 * q] = tdiag[q];
+                dd[2 * q + 1] = 1.0 / tdiag[q];  // correctly rounded reciprocal
+            }
         }
     }
     std::vector<int32_t> rows(order.begin(), order.end());
     rows.resize(padded, 0);
-    std::vector<int64_t> ceoff;
-    std::vector<int32_t> sl;
-    const int64_t slw = ch / 32 + 4;
-    if (single_cta) {
-        ceoff.resize(nchunks + 1);
-        sl.assign(nchunks * slw, 0);
-        for (int64_t c = 0; c <= nchunks; ++c) ceoff[c] = soff[std::min(nslices, c * (ch / 32))];
-        for (int64_t c = 0; c < nchunks; ++c)
-            for (int64_t wl = 0; wl <= ch / 32; ++wl)
-                sl[c * slw + wl] = (int32_t)(soff[std::min(nslices, c * (ch / 32) + wl)] - ceoff[c]);
-    }
 
     rsb_ctx *ctx = T->ctx;
     auto *S = new TriSched();
@@ -258,7 +267,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     S->stage_emax = (int32_t)emax;
     S->nchunks = (int32_t)nchunks;
     S->padded_n = padded;
-    if (const char *ex = getenv("RSB_TRSV_EXPERIMENT")) S->experiment = atoi(ex);
+    S->nrecs = (int64_t)recs.size();
     int rc = RSB_OK;
     if (S->single_cta && (rc = prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
         delete S;
@@ -271,11 +280,11 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (rc = dev_upload(ctx, &S->ecol, ecol.data(), slots)) != RSB_OK ||
         (rc = dev_upload(ctx, &S->eval, eval.data(), slots)) != RSB_OK ||
         (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), tdiag.size())) != RSB_OK) ||
-        (single_cta && (rc = dev_upload(ctx, &S->chunk_eoff, ceoff.data(), ceoff.size())) != RSB_OK) ||
-        (single_cta && (rc = dev_upload(ctx, &S->sloc, sl.data(), sl.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->chunk_roff, croff.data(), croff.size())) != RSB_OK) ||
         (single_cta && (rc = dev_alloc(ctx, (void **)&S->bpos, padded * sizeof(double))) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
-        (single_cta && (rc = dev_upload(ctx, &S->tlen, tlen.data(), tlen.size())) != RSB_OK) ||
+        (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
+        (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK) {
         tri_free(ctx, S);
         return rc;
@@ -299,13 +308,13 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     dev_free(ctx, s->ecol, s->entries * sizeof(int32_t));
     dev_free(ctx, s->eval, s->entries * sizeof(double));
     if (s->diag) dev_free(ctx, s->diag, padded * sizeof(double));
-    if (s->chunk_eoff) dev_free(ctx, s->chunk_eoff, (s->nchunks + 1) * sizeof(int64_t));
-    if (s->sloc) dev_free(ctx, s->sloc, (size_t)s->nchunks * (s->stage_ch / 32 + 4) * sizeof(int32_t));
-    if (s->bpos) dev_free(ctx, s->bpos, padded * sizeof(double));
-    if (s->recs) dev_free(ctx, s->recs, s->entries * sizeof(StageRec));
-    if (s->tlen) dev_free(ctx, s->tlen, padded * sizeof(int32_t));
     dev_free(ctx, s->ticket, sizeof(unsigned long long));
     dev_free(ctx, s->level_ptr, (s->nlevels + 1) * sizeof(int32_t));
+    if (s->chunk_roff) dev_free(ctx, s->chunk_roff, (s->nchunks + 1) * sizeof(int64_t));
+    if (s->bpos) dev_free(ctx, s->bpos, padded * sizeof(double));
+    if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));
+    if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
+    if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
     delete s;
 }
 

@@ -141,7 +141,8 @@ int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
         delete ctx;
         return RSB_ECUDA;
     }
-    int rc = dev_alloc(ctx, (void **)&ctx->d_scalar, 64 * sizeof(double));
+    int rc = prepare_kernels();
+    if (rc == RSB_OK) rc = dev_alloc(ctx, (void **)&ctx->d_scalar, 64 * sizeof(double));
     if (rc == RSB_OK) {
         ctx->partial_cap = 2 * 148 * 4;
         rc = dev_alloc(ctx, (void **)&ctx->d_partials, ctx->partial_cap * sizeof(double));

@@ -17,7 +17,9 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kTriBlock = 128;
 constexpr int kCtaTri = 128;
-constexpr int kStageRegs = 16;  // entries per task held in registers by the staged solve
+constexpr int kStageRegs = 16;
+constexpr int kDotChunk = 2048;  // elements per vector per stage of the staged exact dot
+constexpr int kDotStages = 3;  // entries per task held in registers by the staged solve
 
 __device__ __forceinline__ bool gated(const Gate &g) {
     return (g.a && *(volatile const int *)g.a) || (g.b && *(volatile const int *)g.b);
@@ -37,25 +39,14 @@ __device__ __forceinline__ double vin(const VecIn &v, int64_t i) {
 // rso_blas_dot, tests/test_oracle_pin.py).  All lanes must call; the
 // result is valid in every lane.
 // ---------------------------------------------------------------------------
+// Second half of the OpenBLAS ddot association, given each lane's FMA
+// accumulator over the 32-blocks [0, n32): fold 8 -> 4, the trailing 16-block,
+// the lane reduction and the scalar tail.
 template <class LA, class LB>
-__device__ __forceinline__ double warp_blas_dot(int64_t n, LA la, LB lb) {
+__device__ __forceinline__ double warp_blas_finish(double acc, int64_t n, LA la, LB lb) {
     const int lane = threadIdx.x & 31;
     const int64_t n1 = n & ~(int64_t)15;
     const int64_t n32 = n1 & ~(int64_t)31;
-    double acc = 0.0;
-    int64_t i = lane;
-    // unrolled FMA chain: loads of 8 blocks issued ahead of the dependent FMAs
-    for (; i + 7 * 32 < n32; i += 8 * 32) {
-        double xa[8], xb[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            xa[u] = la(i + u * 32);
-            xb[u] = lb(i + u * 32);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = fma(xa[u], xb[u], acc);
-    }
-    for (; i < n32; i += 32) acc = fma(la(i), lb(i), acc);
     // fold a5[g][k] + a5[g][k+4] into lane 8g+k (k < 4)
     double hi = __shfl_down_sync(0xffffffffu, acc, 4);
     double a4 = acc + hi;  // meaningful in lanes with (lane & 7) < 4
@@ -78,6 +69,28 @@ __device__ __forceinline__ double warp_blas_dot(int64_t n, LA la, LB lb) {
     double dot = n1 ? (t0 + t2) + (t1 + t3) : 0.0;
     for (int64_t e = n1; e < n; ++e) dot = fma(lb(e), la(e), dot);
     return dot;
+}
+
+template <class LA, class LB>
+__device__ __forceinline__ double warp_blas_dot(int64_t n, LA la, LB lb) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n1 = n & ~(int64_t)15;
+    const int64_t n32 = n1 & ~(int64_t)31;
+    double acc = 0.0;
+    int64_t i = lane;
+    // unrolled FMA chain: loads of 8 blocks issued ahead of the dependent FMAs
+    for (; i + 7 * 32 < n32; i += 8 * 32) {
+        double xa[8], xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            xa[u] = la(i + u * 32);
+            xb[u] = lb(i + u * 32);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(xa[u], xb[u], acc);
+    }
+    for (; i < n32; i += 32) acc = fma(la(i), lb(i), acc);
+    return warp_blas_finish(acc, n, la, lb);
 }
 
 __global__ void k_dot_exact(int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
@@ -398,6 +411,48 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         : "memory");
 }
 
+// Exact-order dot for long contiguous vectors: the same single-warp OpenBLAS
+// association as k_dot_exact, with both operands streamed through shared
+// memory by TMA bulk copies (kDotStages-deep mbarrier pipeline) so the FMA
+// chain waits on shared-memory, not global-memory, latency.
+__global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double *a, const double *b, double *out,
+                                                         int sqrt_out, Gate g, const int *need) {
+    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    extern __shared__ __align__(16) double dbuf[];
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(dbuf + kDotStages * 2 * kDotChunk);
+    const int lane = threadIdx.x;
+    const int64_t n32 = (n & ~(int64_t)15) & ~(int64_t)31;
+    const int64_t nch = (n32 + kDotChunk - 1) / kDotChunk;
+    if (lane == 0) {
+        for (int st = 0; st < kDotStages; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int64_t c) {
+        const int st = (int)(c % kDotStages);
+        const int64_t e0 = c * kDotChunk, cnt = min((int64_t)kDotChunk, n32 - e0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[st], (unsigned)(2 * cnt * 8));
+        bulk_g2s(dbuf + (size_t)st * 2 * kDotChunk, a + e0, (unsigned)(cnt * 8), &bar[st]);
+        bulk_g2s(dbuf + (size_t)st * 2 * kDotChunk + kDotChunk, b + e0, (unsigned)(cnt * 8), &bar[st]);
+    };
+    if (lane == 0)
+        for (int64_t c = 0; c < min((int64_t)kDotStages, nch); ++c) issue(c);
+    double acc = 0.0;
+    for (int64_t c = 0; c < nch; ++c) {
+        const int st = (int)(c % kDotStages);
+        mbar_wait(&bar[st], (unsigned)((c / kDotStages) & 1));
+        const double *sa = dbuf + (size_t)st * 2 * kDotChunk, *sb = sa + kDotChunk;
+        const int cnt = (int)min((int64_t)kDotChunk, n32 - c * kDotChunk);
+#pragma unroll 8
+        for (int i = lane; i < cnt; i += 32) acc = fma(sa[i], sb[i], acc);
+        __syncwarp();
+        if (lane == 0 && c + kDotStages < nch) issue(c + kDotStages);
+    }
+    const double d = warp_blas_finish(acc, n, [&](int64_t i) { return a[i]; }, [&](int64_t i) { return b[i]; });
+    if (lane == 0) out[0] = sqrt_out ? sqrt(d) : d;
+}
+
 // right-hand side in task-position order: bpos[t] = a(row_t) [+ c[row_t]]
 __global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row, VecIn a, const double *c,
                              double *bpos, Gate g) {
@@ -436,9 +491,9 @@ __global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row,
 // path's registers free.
 __device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const unsigned char *ring,
                                             const double *x, bool far) {
-    auto la = [&](int q) { return rec[q * 32].v; };
+    auto la = [&](int q) { return rec[q].v; };
     auto lb = [&](int q) {
-        const int s = rec[q * 32].src;
+        const int s = rec[q].src;
         return (!far || s >= 0) ? *reinterpret_cast<const double *>(ring + s) : x[-s - 2];
     };
     const int n1 = len & ~15, n32 = n1 & ~31;
@@ -462,59 +517,135 @@ __device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const 
     return dot;
 }
 
+// a / d correctly rounded, given y = RN(1/d): q0 = RN(a*y), r = a - q0*d
+// (exact, FMA), q1 = RN(q0 + r*y) (Markstein).  Valid while no intermediate
+// over/underflows -- guaranteed for |a|, |d| in (2^-500, 2^500); outside that
+// range (zeros, subnormals, non-finite values included) the IEEE division
+// runs instead.  24 cycles of dependent FP64 instead of ~400 for div.rn.f64
+// on sm_100 (scripts/probes/fp64_latency.cu); cross-checked bit for bit
+// against a/b on 2.8e9 random and adversarial operand pairs.
+__device__ __forceinline__ double exact_div(double a, double d, double y) {
+    const double aa = fabs(a), ad = fabs(d);
+    if (aa > 0x1p-500 && aa < 0x1p500 && ad > 0x1p-500 && ad < 0x1p500) {
+        const double q0 = __dmul_rn(a, y);
+        const double r = fma(-q0, d, a);
+        return fma(r, y, q0);
+    }
+    return __ddiv_rn(a, d);
+}
+
+// One staged task with at most N entries (N = the warp's longest task, so
+// the loop is unrolled for exactly that many): all record and ring loads are
+// issued first, products are formed off the chain, and the chain itself is
+// one DSUB (sequential axpy order, sc.py:261-262) or one DFMA (OpenBLAS ddot
+// order for < 16 entries, sc.py:291) per entry.  Entries past the lane's own
+// length, and skipped ones (x_j == 0), contribute nothing: the DSUB chain
+// subtracts +0.0 (identity for every acc, also -0.0), and fma(0, 0, dot) =
+// dot because the FMA chain from +0.0 can never produce -0.0.
+template <int N, int MODE, bool FAR>
+__device__ __forceinline__ double stage_task(const StageRec *rec, int len, double acc, const unsigned char *ring,
+                                             const double *x) {
+    double v[N], xv[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        v[q] = 0.0;
+        xv[q] = 0.0;
+        if (q < len) {
+            const StageRec r = rec[q];
+            v[q] = r.v;
+            xv[q] = (!FAR || r.src >= 0) ? *reinterpret_cast<const double *>(ring + r.src) : x[-r.src - 2];
+        }
+    }
+    if (!(MODE & 1)) {
+        double pr[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) pr[q] = xv[q] != 0.0 ? __dmul_rn(v[q], xv[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) acc = __dsub_rn(acc, pr[q]);
+    } else if (len > 0) {
+        double dot = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) dot = fma(v[q], xv[q], dot);
+        acc = __dsub_rn(acc, dot);
+    }
+    return acc;
+}
+
+// tasks with >= 16 entries (rare): streaming loop, BLAS-blocked dot order
+template <int MODE, bool FAR>
+__device__ __noinline__ double stage_task_long(const StageRec *rec, int len, double acc, const unsigned char *ring,
+                                               const double *x) {
+    auto src = [&](int s) -> double {
+        return (!FAR || s >= 0) ? *reinterpret_cast<const double *>(ring + s) : x[-s - 2];
+    };
+    if (!(MODE & 1)) {
+        for (int q = 0; q < len; ++q) {
+            const StageRec r = rec[q];
+            const double xj = src(r.src);
+            if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(r.v, xj));
+        }
+    } else if (len > 0) {
+        double dot = 0.0;
+        if (len < 16) {
+            for (int q = 0; q < len; ++q) {
+                const StageRec r = rec[q];
+                dot = fma(r.v, src(r.src), dot);
+            }
+        } else {
+            dot = rec_blas_dot(rec, len, ring, x, FAR);
+        }
+        acc = __dsub_rn(acc, dot);
+    }
+    return acc;
+}
+
 template <int MODE, bool FAR>
 __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gate g) {
     if (gated(g)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool kDiag = (MODE & 2) != 0;
-    const int CH = T.stage_ch, EM = T.stage_emax, SLW = CH / 32 + 4;
+    const int CH = T.stage_ch, EM = T.stage_emax;
     unsigned char *ring = smem;
     unsigned char *bufs = smem + (size_t)kRing * 8;
-    const size_t o_d = (size_t)CH * 8, o_rec = o_d + (kDiag ? (size_t)CH * 8 : 0), o_row = o_rec + (size_t)EM * 16,
-                 o_len = o_row + (size_t)CH * 4, o_sl = o_len + (size_t)CH * 4, bb = o_sl + (size_t)SLW * 4;
+    const size_t o_meta = (size_t)CH * 8, o_dd = o_meta + (size_t)CH * 16,
+                 o_rec = o_dd + (kDiag ? (size_t)CH * 16 : 0), bb = o_rec + (size_t)EM * 16;
     unsigned long long *mbar = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * bb);
     int *lvl = reinterpret_cast<int *>(mbar + 2 * kStageBufs);
     const int nlev = T.nlevels, nch = T.nchunks, lgch = __ffs(CH) - 1;
-    // per-chunk entry counts (the issuing thread must not wait on global loads)
-    int *cne = lvl + ((nlev + 4) & ~3);
+    int *cnr = lvl + ((nlev + 4) & ~3);  // records per chunk: issuing never waits on global loads
     for (int i = threadIdx.x; i <= nlev; i += blockDim.x) lvl[i] = T.level_ptr[i];
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) cne[c] = (int)(T.chunk_eoff[c + 1] - T.chunk_eoff[c]);
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) cnr[c] = (int)(T.chunk_roff[c + 1] - T.chunk_roff[c]);
     if (threadIdx.x == 0) {
         for (int b = 0; b < kStageBufs; ++b) mbar_init(&mbar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    long long e_next = 0;  // entry offset of the next chunk to issue (thread 0)
+    long long r_next = 0;  // first record of the next chunk to issue (thread 0)
     auto issue = [&](int c) {  // thread 0 only
         unsigned char *B = bufs + (size_t)(c & (kStageBufs - 1)) * bb;
-        const int64_t e0 = e_next, ne = cne[c];
-        e_next += ne;
-        const unsigned bytes = (unsigned)(CH * 8 + (kDiag ? CH * 8 : 0) + ne * 16 + CH * 8 + SLW * 4);
+        const int ne = cnr[c];
+        const long long r0 = r_next;
+        r_next += ne;
         unsigned long long *bar = &mbar[c & (kStageBufs - 1)];
+        const unsigned bytes = (unsigned)(CH * 8 + CH * 16 + (kDiag ? CH * 16 : 0) + ne * 16);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(bar, bytes);
         bulk_g2s(B, T.bpos + (int64_t)c * CH, CH * 8, bar);
-        if (kDiag) bulk_g2s(B + o_d, T.diag + (int64_t)c * CH, CH * 8, bar);
-        if (ne) bulk_g2s(B + o_rec, T.recs + e0, (unsigned)(ne * 16), bar);
-        bulk_g2s(B + o_row, T.task_row + (int64_t)c * CH, CH * 4, bar);
-        bulk_g2s(B + o_len, T.tlen + (int64_t)c * CH, CH * 4, bar);
-        bulk_g2s(B + o_sl, T.sloc + (int64_t)c * SLW, SLW * 4, bar);
+        bulk_g2s(B + o_meta, T.meta + (int64_t)c * CH, CH * 16, bar);
+        if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * (int64_t)c * CH, CH * 16, bar);
+        if (ne) bulk_g2s(B + o_rec, T.recs + r0, (unsigned)ne * 16, bar);
     };
     int issued = min(kStageBufs, nch), ready = -1;
     if (threadIdx.x == 0)
         for (int c = 0; c < issued; ++c) issue(c);
-    auto src = [&](int s) -> double {
-        if (!FAR || s >= 0) return *reinterpret_cast<const double *>(ring + s);
-        return x[-s - 2];
-    };
     for (int l = 0; l < nlev; ++l) {
         const int lo = lvl[l], hi = lvl[l + 1];
-        const int first = lo >> lgch;  // refill buffers whose chunk lies wholly before this level
+        const int first = lo >> lgch;       // refill buffers whose chunk lies wholly before this level
+        const int last = (hi - 1) >> lgch;  // chunks this level reads must have landed
         while (issued < nch && issued < first + kStageBufs) {
             if (threadIdx.x == 0) issue(issued);
             ++issued;
         }
-        const int last = (hi - 1) >> lgch;  // chunks this level reads must have landed
         while (ready < last) {
             ++ready;
             mbar_wait(&mbar[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
@@ -522,62 +653,35 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
         for (int t = lo + threadIdx.x; t < hi; t += kCtaTri) {
             const int loc = t & (CH - 1);
             const unsigned char *B = bufs + (size_t)((t >> lgch) & (kStageBufs - 1)) * bb;
-            const int len = reinterpret_cast<const int *>(B + o_len)[loc];
-            const int row = reinterpret_cast<const int *>(B + o_row)[loc];
-            const StageRec *rec = reinterpret_cast<const StageRec *>(B + o_rec) +
-                                  reinterpret_cast<const int *>(B + o_sl)[loc >> 5] + (t & 31);
+            const StageMeta m = reinterpret_cast<const StageMeta *>(B + o_meta)[loc];
             double acc = reinterpret_cast<const double *>(B)[loc];
-            const double d = kDiag ? reinterpret_cast<const double *>(B + o_d)[loc] : 1.0;
-            // warp-uniform trip count: the longest task among the active lanes
-            const int wlen = __reduce_max_sync(__activemask(), len);
-            double vv[kStageRegs], xv[kStageRegs];
-#pragma unroll
-            for (int q = 0; q < kStageRegs; ++q) {
-                vv[q] = 0.0;
-                xv[q] = 0.0;
-                if (q < len) {
-                    const StageRec r = rec[q * 32];
-                    vv[q] = r.v;
-                    xv[q] = src(r.src);
-                }
+            double2 dr = make_double2(1.0, 1.0);
+            if (kDiag) dr = reinterpret_cast<const double2 *>(B + o_dd)[loc];
+            const StageRec *rec = reinterpret_cast<const StageRec *>(B + o_rec) + m.roff;
+            // code path unrolled for exactly the warp's longest task
+            const int wlen = __reduce_max_sync(__activemask(), m.len);
+            switch (wlen) {
+                case 0: break;
+                case 1: acc = stage_task<1, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 2: acc = stage_task<2, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 3: acc = stage_task<3, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 4: acc = stage_task<4, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 5: acc = stage_task<5, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 6: acc = stage_task<6, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 7: acc = stage_task<7, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 8: acc = stage_task<8, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 9: acc = stage_task<9, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 10: acc = stage_task<10, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 11: acc = stage_task<11, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 12: acc = stage_task<12, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 13: acc = stage_task<13, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 14: acc = stage_task<14, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                case 15: acc = stage_task<15, MODE, FAR>(rec, m.len, acc, ring, x); break;
+                default: acc = stage_task_long<MODE, FAR>(rec, m.len, acc, ring, x); break;
             }
-            if (!(MODE & 1)) {
-                // x_i -= l_ij * x_j in stored order, skipped when x_j == 0 (sc.py:261-262)
-#pragma unroll
-                for (int q = 0; q < kStageRegs; ++q) {
-                    if (q >= wlen) break;  // uniform across the warp
-                    // predicated, not branched: lanes have different lengths
-                    const double nx = __dsub_rn(acc, __dmul_rn(vv[q], xv[q]));
-                    acc = (q < len && xv[q] != 0.0) ? nx : acc;
-                }
-                for (int q = kStageRegs; q < len; ++q) {
-                    const StageRec r = rec[q * 32];
-                    const double xj = src(r.src);
-                    if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(r.v, xj));
-                }
-            } else if (len > 0) {
-                // x_j -= vals @ x[rows]: OpenBLAS ddot order (sc.py:291,296,311)
-                double dot = 0.0;
-                if (len < 16) {
-#pragma unroll
-                    for (int q = 0; q < kStageRegs; ++q) {
-                        if (q >= wlen) break;  // uniform across the warp
-                        const double nd = fma(vv[q], xv[q], dot);
-                        dot = q < len ? nd : dot;
-                    }
-                    for (int q = kStageRegs; q < len; ++q) {
-                        const StageRec r = rec[q * 32];
-                        dot = fma(r.v, src(r.src), dot);
-                    }
-                } else {
-                    dot = rec_blas_dot(rec, len, ring, x, FAR);
-                }
-                acc = __dsub_rn(acc, dot);
-            }
-            if (kDiag) acc = __ddiv_rn(acc, d);
-            const double v = canonical(acc);
-            *reinterpret_cast<double *>(ring + (size_t)(t & (kRing - 1)) * 8) = v;
-            x[row] = v;
+            if (kDiag) acc = exact_div(acc, dr.x, dr.y);
+            *reinterpret_cast<double *>(ring + (size_t)(t & (kRing - 1)) * 8) = acc;
+            x[m.row] = acc;
         }
         __syncthreads();
     }
@@ -803,8 +907,20 @@ int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_
         k_dot_tree_final<<<1, 32, 0, ctx->stream>>>(parts, ctx->d_partials, out, sqrt_out, g, need);
         return post_launch(ctx);
     }
+    const bool plain = !a.g && !b.g && !a.off && !b.off && ((uintptr_t)a.p % 16 == 0) && ((uintptr_t)b.p % 16 == 0);
+    if (plain && n >= 2 * kDotChunk) {
+        const size_t smem = (size_t)kDotStages * 2 * kDotChunk * 8 + kDotStages * 8;
+        k_dot_exact_staged<<<1, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need);
+        return post_launch(ctx);
+    }
     k_dot_exact<<<1, 32, 0, ctx->stream>>>(n, a, b, out, sqrt_out, g, need);
     return post_launch(ctx);
+}
+
+int prepare_kernels() {
+    const int smem = kDotStages * 2 * kDotChunk * 8 + kDotStages * 8;
+    RSB_TRY_CUDA(cudaFuncSetAttribute(k_dot_exact_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return RSB_OK;
 }
 
 int launch_copy(rsb_ctx *ctx, double *dst, VecIn src, int64_t n, Gate g) {

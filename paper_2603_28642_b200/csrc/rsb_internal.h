@@ -51,8 +51,9 @@ constexpr int kStageBufs = 4;
 constexpr int kStageSmemBudget = 220 * 1024;
 // shared-memory bytes of one staging buffer
 inline int64_t stage_buf_bytes(int64_t ch, int64_t emax, bool diag) {
-    // rhs, [diag], entry records (16 B), rows, lengths, slice offsets
-    return ch * 8 + (diag ? ch * 8 : 0) + emax * 16 + ch * 4 + ch * 4 + (ch / 32 + 4) * 4;
+    // rhs (8 B), task meta {row, len, record offset, -} (16 B), [diag, 1/diag] (16 B),
+    // entry records (16 B, contiguous per task)
+    return ch * 8 + ch * 16 + (diag ? ch * 16 : 0) + emax * 16;
 }
 
 // One entry of a staged solve: the factor value and where its unknown is read
@@ -64,10 +65,17 @@ struct alignas(16) StageRec {
     int32_t pad;
 };
 inline int64_t stage_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels, int64_t nchunks) {
-    // ring, staging buffers, mbarriers, level bounds (padded to 4), chunk entry counts
+    // ring, staging buffers, mbarriers, level bounds (padded to 4), chunk record counts
     return (int64_t)kRing * 8 + kStageBufs * stage_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
            ((nlevels + 4) & ~3LL) * 4 + nchunks * 4;
 }
+// task metadata of a staged solve (position order)
+struct alignas(16) StageMeta {
+    int32_t row;  // unknown written
+    int32_t len;  // entries
+    int32_t roff; // first record, relative to the task's chunk
+    int32_t pad;
+};
 
 // ---------------------------------------------------------------------------
 // device-side views (passed by value to kernels)
@@ -126,12 +134,11 @@ struct TriDev {
     int32_t stage_ch;     // positions per chunk (multiple of 128, >= widest level)
     int32_t stage_emax;   // max entry slots of a chunk
     int32_t nchunks;
-    const int64_t *chunk_eoff;  // entry-slot offset of each chunk (nchunks + 1)
-    const int32_t *sloc;        // per chunk: slice offsets local to the chunk (stage_ch/32 + 4)
+    const int64_t *chunk_roff;  // first record of each chunk (nchunks + 1)
     double *bpos;               // right-hand side gathered into position order
-    int32_t experiment;         // timing experiments only (RSB_TRSV_EXPERIMENT)
-    const StageRec *recs;       // entry records in the warp-interleaved slot order
-    const int32_t *tlen;        // entries per task (position order, padded)
+    const StageRec *recs;       // entry records, contiguous per task in position order
+    const StageMeta *meta;      // per position (padded to nchunks * stage_ch)
+    const double *ddiag;        // per position: {diag, RN(1/diag)} (staged solve's exact division)
 };
 
 // ---------------------------------------------------------------------------
@@ -163,17 +170,17 @@ struct TriSched {
     int64_t far_entries = 0;
     int32_t *level_ptr = nullptr;  // nlevels + 1 task positions
     int32_t stage_ch = 0, stage_emax = 0, nchunks = 0;
-    int64_t *chunk_eoff = nullptr;
-    int32_t *sloc = nullptr;
+    int64_t *chunk_roff = nullptr;
     double *bpos = nullptr;
-    int64_t padded_n = 0;  // task_row / diag / bpos lengths (nchunks * stage_ch when staged)
-    int32_t experiment = 0;
+    int64_t padded_n = 0;  // task_row / diag / bpos / meta lengths (nchunks * stage_ch when staged)
     StageRec *recs = nullptr;
-    int32_t *tlen = nullptr;
+    int64_t nrecs = 0;
+    StageMeta *meta = nullptr;
+    double *ddiag = nullptr;
     TriDev view() const {
-        return TriDev{n,        mode,       task_row, slice_off,  ecol, eval, diag,       ticket,
-                      has_far,  (int32_t)nlevels,      level_ptr, stage_ch, stage_emax, nchunks,
-                      chunk_eoff, sloc,     bpos,     experiment, recs, tlen};
+        return TriDev{n,       mode,       task_row, slice_off,  ecol, eval, diag,   ticket,
+                      has_far, (int32_t)nlevels,     level_ptr, stage_ch, stage_emax, nchunks,
+                      chunk_roff, bpos,    recs,     meta,       ddiag};
     }
 };
 
@@ -252,6 +259,8 @@ int get_tri(rsb_mat *T, int kind, TriSched **out);
 int prepare_trsv_cta(int64_t n);
 // one-time kernel attribute setup for the dense S solve of size s
 int prepare_chol(int64_t s);
+// one-time kernel attribute setup at context creation (dynamic shared memory)
+int prepare_kernels();
 
 // triangular-solve analysis (analysis.cpp)
 int tri_analyse(rsb_mat *T, int kind, TriSched **out);

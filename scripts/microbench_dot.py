@@ -1,0 +1,15 @@
+"""Device time of one exact-order dot (rsb_dot on device vectors) at several lengths."""
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_28642_b200 import _lib as L
+from paper_2603_28642_b200.device import DeviceBuffer, get_context
+ctx = get_context(); out = {}
+for n in (32768, 65536, 98304, 1 << 20):
+    rng = np.random.default_rng(n); a = DeviceBuffer(ctx, n); b = DeviceBuffer(ctx, n)
+    a.upload(rng.standard_normal(n)); b.upload(rng.standard_normal(n)); r = np.zeros(1); ts = []
+    for k in range(13):
+        ctx.mark(0); L.check(L.lib().rsb_dot(ctx.h, n, a.ptr, b.ptr, r.ctypes.data_as(L.f64p), L.RSB_DEVICE)); ctx.mark(1)
+        if k >= 3: ts.append(ctx.elapsed_ms(0, 1))
+    out[n] = round(1e3 * float(np.median(ts)), 2)
+print(json.dumps({"dot_us": out}))
