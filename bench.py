@@ -206,13 +206,14 @@ def measured_peak():
 
 
 def ncu_traffic():
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture (profiles/ncu_trsv_summary.json), or None."""
-    path = os.path.join(HERE, "profiles", "ncu_trsv_summary.json")
+    """DRAM bytes (read + write) per iteration of the dominant kernel class,
+    summed over the iteration's solves, from the committed ncu capture
+    (profiles/ncu_trsv_r01.json), or None."""
+    path = os.path.join(HERE, "profiles", "ncu_trsv_r01.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_launch_by_factor"), d.get("source")
+        return d.get("dram_bytes_per_iteration"), d.get("source")
     except (OSError, ValueError):
         return None, None
 
@@ -398,7 +399,8 @@ def run_b200(args):
             "dot_order": "exact (reference OpenBLAS association)",
         },
         "roofline": {
-            "kernel": "k_trsv (sync-free level-ordered triangular solves, incl. sentinel fill)",
+            "kernel": "k_trsv_stage (+ k_gather_pos): level-synchronous single-CTA triangular solves, "
+                      "8 per cg(2) iteration",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
             "traffic_source": traffic_src,
