@@ -105,6 +105,9 @@ int rsb_matvec_transpose(rsb_mat *A, const double *y, double *z, int where);
 /* triangular solves, kind = RSB_TRI_*  (sc.py:243-313).  Level analysis is
  * done on first use per (matrix, kind) and cached on the matrix. */
 int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where);
+/* diagnostics: per-phase cycle counters of the last staged solve of (matrix,
+ * kind); only when the schedule was analysed with RSB_TRSV_PROFILE set */
+int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters);
 /* dependency levels of the (matrix, kind) solve DAG (analysing it if needed) */
 int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
 /* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),

@@ -169,18 +169,39 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     bool single_cta = n <= kCtaTriMaxN && (n / std::max<int64_t>(1, nlev)) <= kCtaTriMaxMeanWidth;
     if (force && std::strcmp(force, "grid") == 0) single_cta = false;
     if (force && std::strcmp(force, "cta") == 0 && n <= kCtaTriMaxN) single_cta = true;
-    // records per position (contiguous per task) and their prefix sums
-    std::vector<int64_t> rpre;
-    int64_t ch = 0, emax = 0;
+    // staged position space: every level padded to whole 32-task slices, so a
+    // warp's 32 lanes are one slice of one level; records are lane-interleaved
+    // per slice (entry q of lane l at slice_base + 32q + l, conflict-free
+    // 16-byte shared loads) with the slice's longest task as its trip count
+    std::vector<int64_t> sp;     // staged start of each level (multiple of 32)
+    std::vector<int64_t> srb;    // record base of each staged slice (prefix sums of 32 * K)
+    int64_t ch = 0, emax = 0, ns = 0, maxw32 = 0;
     if (single_cta) {
-        rpre.assign(n + 1, 0);
-        for (int64_t q = 0; q < n; ++q) rpre[q + 1] = rpre[q] + (tptr[order[q] + 1] - tptr[order[q]]);
+        sp.assign(nlev + 1, 0);
+        for (int32_t l = 0; l < nlev; ++l) {
+            const int64_t w = lstart[l + 1] - lstart[l];
+            sp[l + 1] = sp[l] + (w + 31) / 32 * 32;
+            maxw32 = std::max(maxw32, (w + 31) / 32 * 32);
+        }
+        ns = sp[nlev];
+        const int64_t nsl = ns / 32;
+        srb.assign(nsl + 1, 0);
+        for (int32_t l = 0; l < nlev; ++l)
+            for (int64_t q0 = sp[l]; q0 < sp[l + 1]; q0 += 32) {
+                int64_t K = 0;
+                for (int64_t q = q0; q < q0 + 32; ++q) {
+                    const int64_t src_q = lstart[l] + (q - sp[l]);
+                    if (src_q < lstart[l + 1]) K = std::max(K, tptr[order[src_q] + 1] - tptr[order[src_q]]);
+                }
+                srb[q0 / 32 + 1] = 32 * K;
+            }
+        for (int64_t w = 0; w < nsl; ++w) srb[w + 1] += srb[w];
         for (int64_t cand : {1024, 512, 256, 128}) {
-            if (cand < maxw) break;
+            if (cand < maxw32) break;
             int64_t em = 0;
-            for (int64_t c0 = 0; c0 < n; c0 += cand) em = std::max(em, rpre[std::min(n, c0 + cand)] - rpre[c0]);
-            em = std::max<int64_t>(2, (em + 1) & ~1LL);
-            if (stage_smem_bytes(cand, em, !unit, nlev, (n + cand - 1) / cand) <= kStageSmemBudget) {
+            for (int64_t c0 = 0; c0 < ns; c0 += cand) em = std::max(em, srb[std::min(ns, c0 + cand) / 32] - srb[c0 / 32]);
+            em = std::max<int64_t>(32, em);
+            if (stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand) <= kStageSmemBudget) {
                 ch = cand;
                 emax = em;
                 break;
@@ -188,15 +209,16 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         }
         if (ch == 0) single_cta = false;
     }
-    std::vector<int32_t> posof;
+    std::vector<int32_t> posof;  // staged position of each unknown
     if (single_cta) {
         posof.resize(n);
-        for (int64_t q = 0; q < n; ++q) posof[order[q]] = (int32_t)q;
+        for (int32_t l = 0; l < nlev; ++l)
+            for (int64_t q = lstart[l]; q < lstart[l + 1]; ++q) posof[order[q]] = (int32_t)(sp[l] + (q - lstart[l]));
     }
 
     std::vector<int32_t> ecol(slots, -1);
     std::vector<double> eval(slots, 0.0);
-    const int64_t nchunks = single_cta ? (n + ch - 1) / ch : 0;
+    const int64_t nchunks = single_cta ? (ns + ch - 1) / ch : 0;
     const int64_t padded = single_cta ? nchunks * ch : n;
     std::vector<double> tdiag;
     if (!unit) tdiag.assign(padded, 1.0);
@@ -212,45 +234,56 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             if (!unit) tdiag[q] = diag[t];
         }
     }
-    // staged layout: per-position meta, {diag, 1/diag}, contiguous records whose
-    // source is the ring byte offset of a live dependency or -(row + 2)
+    // staged layout: per-position meta, {diag, 1/diag}, lane-interleaved records
+    // whose source is the ring byte offset of a live dependency or -(row + 2)
     std::vector<StageRec> recs;
     std::vector<StageMeta> meta;
     std::vector<double> dd;
     std::vector<int64_t> croff;
+    std::vector<int32_t> srows;
     int64_t far = 0;
     if (single_cta) {
-        recs.resize(std::max<int64_t>(2, rpre[n]));
-        meta.assign(padded, StageMeta{0, 0, 0, 0});
+        recs.assign(std::max<int64_t>(32, srb[ns / 32]), StageRec{0.0, 0, 0});
+        meta.assign(padded, StageMeta{-1, 0, 0, 0});
+        srows.assign(padded, -1);
         croff.resize(nchunks + 1);
-        for (int64_t c = 0; c <= nchunks; ++c) croff[c] = rpre[std::min(n, c * ch)];
-        for (int64_t q = 0; q < n; ++q) {
-            const int32_t t = order[q];
-            const int64_t r0 = rpre[q];
-            for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
-                const int32_t col = ent[k].col;
-                const int64_t p = posof[col];
-                int32_t src;
-                if (q - p + maxw < kRing) {
-                    src = (int32_t)((p & (kRing - 1)) * 8);
-                } else {
-                    src = -(col + 2);
-                    ++far;
+        for (int64_t c = 0; c <= nchunks; ++c) croff[c] = srb[std::min(ns, c * ch) / 32];
+        dd.assign(2 * padded, 1.0);
+        for (int32_t l = 0; l < nlev; ++l) {
+            for (int64_t q = sp[l]; q < sp[l + 1]; ++q) {
+                const int64_t sl = q / 32, lane = q & 31;
+                const int32_t K = (int32_t)((srb[sl + 1] - srb[sl]) / 32);
+                const int32_t roff = (int32_t)(srb[sl] - croff[q / ch] + lane);
+                const int64_t gq = lstart[l] + (q - sp[l]);
+                if (gq >= lstart[l + 1]) {  // padding task
+                    meta[q] = StageMeta{-1, 0, roff, K};
+                    continue;
                 }
-                recs[r0 + (k - tptr[t])] = StageRec{ent[k].val, src, 0};
-            }
-            meta[q] = StageMeta{t, (int32_t)(tptr[t + 1] - tptr[t]), (int32_t)(r0 - croff[q / ch]), 0};
-        }
-        if (!unit) {
-            dd.assign(2 * padded, 1.0);
-            for (int64_t q = 0; q < padded; ++q) {
-                dd[2 * q] = tdiag[q];
-                dd[2 * q + 1] = 1.0 / tdiag[q];  // correctly rounded reciprocal
+                const int32_t t = order[gq];
+                for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
+                    const int32_t col = ent[k].col;
+                    const int64_t p = posof[col];
+                    int32_t src;
+                    if (q - p + maxw32 < kRing) {
+                        src = (int32_t)((p & (kRing - 1)) * 8);
+                    } else {
+                        src = -(col + 2);
+                        ++far;
+                    }
+                    recs[srb[sl] + (k - tptr[t]) * 32 + lane] = StageRec{ent[k].val, src, 0};
+                }
+                meta[q] = StageMeta{t, (int32_t)(tptr[t + 1] - tptr[t]), roff, K};
+                srows[q] = t;
+                if (!unit) {
+                    dd[2 * q] = diag[t];
+                    dd[2 * q + 1] = 1.0 / diag[t];  // correctly rounded reciprocal
+                }
             }
         }
     }
     std::vector<int32_t> rows(order.begin(), order.end());
     rows.resize(padded, 0);
+    if (single_cta) rows = srows;  // the staged kernel's gather uses staged positions
 
     rsb_ctx *ctx = T->ctx;
     auto *S = new TriSched();
@@ -274,6 +307,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         return rc;
     }
     std::vector<int32_t> lptr(lstart.begin(), lstart.end());
+    if (single_cta) lptr.assign(sp.begin(), sp.end());
     if ((rc = dev_upload(ctx, &S->level_ptr, lptr.data(), lptr.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->task_row, rows.data(), rows.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->slice_off, soff.data(), nslices + 1)) != RSB_OK ||
@@ -285,7 +319,8 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (single_cta && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
-        (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK) {
+        (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
+        (getenv("RSB_TRSV_PROFILE") && (rc = dev_alloc(ctx, (void **)&S->prof, 8 * sizeof(long long))) != RSB_OK)) {
         tri_free(ctx, S);
         return rc;
     }
@@ -315,6 +350,7 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));
     if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
     if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
+    if (s->prof) dev_free(ctx, s->prof, 8 * sizeof(long long));
     delete s;
 }
 

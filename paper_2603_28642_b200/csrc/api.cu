@@ -370,6 +370,19 @@ int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where) {
     return finish_out(ctx, x, T->ncols, where, sx);
 }
 
+int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters) {
+    TriSched *S = nullptr;
+    RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
+    RSB_TRY(get_tri(T, kind, &S));
+    if (!S->prof) {
+        set_error("triangular schedule was analysed without RSB_TRSV_PROFILE");
+        return RSB_ESTATE;
+    }
+    RSB_TRY_CUDA(cudaMemcpyAsync(counters, S->prof, 8 * sizeof(long long), cudaMemcpyDeviceToHost, T->ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(T->ctx->stream));
+    return RSB_OK;
+}
+
 int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width) {
     TriSched *S = nullptr;
     RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));

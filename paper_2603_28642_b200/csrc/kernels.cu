@@ -459,8 +459,8 @@ __global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row,
     if (gated(g)) return;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < padded; t += (int64_t)gridDim.x * blockDim.x) {
         double v = 0.0;
-        if (t < n) {
-            const int row = task_row[t];
+        const int row = task_row[t];  // -1: padding task of the staged layout
+        if (row >= 0) {
             v = vin(a, row);
             if (c) v = __dadd_rn(v, c[row]);
         }
@@ -491,9 +491,9 @@ __global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row,
 // path's registers free.
 __device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const unsigned char *ring,
                                             const double *x, bool far) {
-    auto la = [&](int q) { return rec[q].v; };
+    auto la = [&](int q) { return rec[q * 32].v; };
     auto lb = [&](int q) {
-        const int s = rec[q].src;
+        const int s = rec[q * 32].src;
         return (!far || s >= 0) ? *reinterpret_cast<const double *>(ring + s) : x[-s - 2];
     };
     const int n1 = len & ~15, n32 = n1 & ~31;
@@ -526,10 +526,13 @@ __device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const 
 // against a/b on 2.8e9 random and adversarial operand pairs.
 __device__ __forceinline__ double exact_div(double a, double d, double y) {
     const double aa = fabs(a), ad = fabs(d);
-    if (aa > 0x1p-500 && aa < 0x1p500 && ad > 0x1p-500 && ad < 0x1p500) {
-        const double q0 = __dmul_rn(a, y);
-        const double r = fma(-q0, d, a);
-        return fma(r, y, q0);
+    if (ad > 0x1p-500 && ad < 0x1p500) {
+        if (aa > 0x1p-500 && aa < 0x1p500) {
+            const double q0 = __dmul_rn(a, y);
+            const double r = fma(-q0, d, a);
+            return fma(r, y, q0);
+        }
+        if (a == 0.0) return __dmul_rn(a, y);  // +-0 with the quotient's sign, exactly as a / d
     }
     return __ddiv_rn(a, d);
 }
@@ -551,7 +554,7 @@ __device__ __forceinline__ double stage_task(const StageRec *rec, int len, doubl
         v[q] = 0.0;
         xv[q] = 0.0;
         if (q < len) {
-            const StageRec r = rec[q];
+            const StageRec r = rec[q * 32];
             v[q] = r.v;
             xv[q] = (!FAR || r.src >= 0) ? *reinterpret_cast<const double *>(ring + r.src) : x[-r.src - 2];
         }
@@ -580,7 +583,7 @@ __device__ __noinline__ double stage_task_long(const StageRec *rec, int len, dou
     };
     if (!(MODE & 1)) {
         for (int q = 0; q < len; ++q) {
-            const StageRec r = rec[q];
+            const StageRec r = rec[q * 32];
             const double xj = src(r.src);
             if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(r.v, xj));
         }
@@ -588,7 +591,7 @@ __device__ __noinline__ double stage_task_long(const StageRec *rec, int len, dou
         double dot = 0.0;
         if (len < 16) {
             for (int q = 0; q < len; ++q) {
-                const StageRec r = rec[q];
+                const StageRec r = rec[q * 32];
                 dot = fma(r.v, src(r.src), dot);
             }
         } else {
@@ -600,56 +603,76 @@ __device__ __noinline__ double stage_task_long(const StageRec *rec, int len, dou
 }
 
 template <int MODE, bool FAR>
-__global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gate g) {
+__global__ void __launch_bounds__(kCtaTri + 32) k_trsv_stage(TriDev T, double *x, Gate g) {
     if (gated(g)) return;
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool kDiag = (MODE & 2) != 0;
+    constexpr int kConsumerWarps = kCtaTri / 32;
     const int CH = T.stage_ch, EM = T.stage_emax;
     unsigned char *ring = smem;
     unsigned char *bufs = smem + (size_t)kRing * 8;
     const size_t o_meta = (size_t)CH * 8, o_dd = o_meta + (size_t)CH * 16,
                  o_rec = o_dd + (kDiag ? (size_t)CH * 16 : 0), bb = o_rec + (size_t)EM * 16;
-    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * bb);
-    int *lvl = reinterpret_cast<int *>(mbar + 2 * kStageBufs);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * bb);
+    unsigned long long *empty = full + kStageBufs;
+    int *lvl = reinterpret_cast<int *>(full + 2 * kStageBufs);
     const int nlev = T.nlevels, nch = T.nchunks, lgch = __ffs(CH) - 1;
-    int *cnr = lvl + ((nlev + 4) & ~3);  // records per chunk: issuing never waits on global loads
     for (int i = threadIdx.x; i <= nlev; i += blockDim.x) lvl[i] = T.level_ptr[i];
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) cnr[c] = (int)(T.chunk_roff[c + 1] - T.chunk_roff[c]);
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kStageBufs; ++b) mbar_init(&mbar[b], 1);
+        for (int b = 0; b < kStageBufs; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], kConsumerWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    long long r_next = 0;  // first record of the next chunk to issue (thread 0)
-    auto issue = [&](int c) {  // thread 0 only
-        unsigned char *B = bufs + (size_t)(c & (kStageBufs - 1)) * bb;
-        const int ne = cnr[c];
-        const long long r0 = r_next;
-        r_next += ne;
-        unsigned long long *bar = &mbar[c & (kStageBufs - 1)];
-        const unsigned bytes = (unsigned)(CH * 8 + CH * 16 + (kDiag ? CH * 16 : 0) + ne * 16);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s(B, T.bpos + (int64_t)c * CH, CH * 8, bar);
-        bulk_g2s(B + o_meta, T.meta + (int64_t)c * CH, CH * 16, bar);
-        if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * (int64_t)c * CH, CH * 16, bar);
-        if (ne) bulk_g2s(B + o_rec, T.recs + r0, (unsigned)ne * 16, bar);
-    };
-    int issued = min(kStageBufs, nch), ready = -1;
-    if (threadIdx.x == 0)
-        for (int c = 0; c < issued; ++c) issue(c);
+    if (threadIdx.x >= kCtaTri) {
+        // producer warp: chunk c goes to buffer c % kStageBufs once the
+        // consumers released the chunk that held it; the consumers never issue
+        if (threadIdx.x == kCtaTri) {
+            for (int c = 0; c < nch; ++c) {
+                const int b = c & (kStageBufs - 1);
+                if (c >= kStageBufs) mbar_wait(&empty[b], (unsigned)(((c / kStageBufs) - 1) & 1));
+                unsigned char *B = bufs + (size_t)b * bb;
+                const int64_t r0 = T.chunk_roff[c];
+                const int ne = (int)(T.chunk_roff[c + 1] - r0);
+                const unsigned bytes = (unsigned)(CH * 8 + CH * 16 + (kDiag ? CH * 16 : 0) + ne * 16);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&full[b], bytes);
+                bulk_g2s(B, T.bpos + (int64_t)c * CH, CH * 8, &full[b]);
+                bulk_g2s(B + o_meta, T.meta + (int64_t)c * CH, CH * 16, &full[b]);
+                if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * (int64_t)c * CH, CH * 16, &full[b]);
+                if (ne) bulk_g2s(B + o_rec, T.recs + r0, (unsigned)ne * 16, &full[b]);
+            }
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    int released = 0, ready = -1;
+    long long pc[7] = {0, 0, 0, 0, 0, 0, 0}, tq = 0, tp = 0;
+    const bool prof = T.prof && threadIdx.x == 0;
+#define RSB_PROF(i)                 \
+    if (prof) {                     \
+        tq = clock64();             \
+        pc[i] += tq - tp;           \
+        tp = tq;                    \
+    }
+    if (prof) tp = clock64();
     for (int l = 0; l < nlev; ++l) {
         const int lo = lvl[l], hi = lvl[l + 1];
         const int first = lo >> lgch;       // refill buffers whose chunk lies wholly before this level
         const int last = (hi - 1) >> lgch;  // chunks this level reads must have landed
-        while (issued < nch && issued < first + kStageBufs) {
-            if (threadIdx.x == 0) issue(issued);
-            ++issued;
-        }
+        for (; released < first; ++released)  // chunks wholly before this level are done
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                 smem_u32(&empty[released & (kStageBufs - 1)]))
+                             : "memory");
+        RSB_PROF(0)
         while (ready < last) {
             ++ready;
-            mbar_wait(&mbar[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
+            mbar_wait(&full[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
         }
+        RSB_PROF(5)
         for (int t = lo + threadIdx.x; t < hi; t += kCtaTri) {
             const int loc = t & (CH - 1);
             const unsigned char *B = bufs + (size_t)((t >> lgch) & (kStageBufs - 1)) * bb;
@@ -658,8 +681,9 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
             double2 dr = make_double2(1.0, 1.0);
             if (kDiag) dr = reinterpret_cast<const double2 *>(B + o_dd)[loc];
             const StageRec *rec = reinterpret_cast<const StageRec *>(B + o_rec) + m.roff;
-            // code path unrolled for exactly the warp's longest task
-            const int wlen = __reduce_max_sync(__activemask(), m.len);
+            RSB_PROF(1)
+            // code path unrolled for exactly the slice's longest task (uniform per warp)
+            const int wlen = m.pad;
             switch (wlen) {
                 case 0: break;
                 case 1: acc = stage_task<1, MODE, FAR>(rec, m.len, acc, ring, x); break;
@@ -679,11 +703,20 @@ __global__ void __launch_bounds__(kCtaTri) k_trsv_stage(TriDev T, double *x, Gat
                 case 15: acc = stage_task<15, MODE, FAR>(rec, m.len, acc, ring, x); break;
                 default: acc = stage_task_long<MODE, FAR>(rec, m.len, acc, ring, x); break;
             }
-            if (kDiag) acc = exact_div(acc, dr.x, dr.y);
+            RSB_PROF(2)
+            if (kDiag && m.row >= 0) acc = exact_div(acc, dr.x, dr.y);
             *reinterpret_cast<double *>(ring + (size_t)(t & (kRing - 1)) * 8) = acc;
-            x[m.row] = acc;
+            if (m.row >= 0) x[m.row] = acc;
+            RSB_PROF(3)
         }
-        __syncthreads();
+        asm volatile("bar.sync 1, %0;" ::"n"(kCtaTri) : "memory");  // consumers only
+        RSB_PROF(4)
+    }
+#undef RSB_PROF
+    if (prof) {
+        for (int i = 0; i < 5; ++i) T.prof[i] = pc[i];
+        T.prof[6] = pc[5];
+        T.prof[5] = nlev;
     }
 }
 
@@ -835,14 +868,14 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         RSB_TRY(post_launch(ctx));
         const int sel = T.mode + (T.has_far ? 4 : 0);
         switch (sel) {
-            case 0: k_trsv_stage<0, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 1: k_trsv_stage<1, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 2: k_trsv_stage<2, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 3: k_trsv_stage<3, false><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 4: k_trsv_stage<0, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 5: k_trsv_stage<1, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            case 6: k_trsv_stage<2, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
-            default: k_trsv_stage<3, true><<<1, kCtaTri, smem, ctx->stream>>>(v, x, g); break;
+            case 0: k_trsv_stage<0, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 1: k_trsv_stage<1, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 2: k_trsv_stage<2, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 3: k_trsv_stage<3, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 4: k_trsv_stage<0, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 5: k_trsv_stage<1, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            case 6: k_trsv_stage<2, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+            default: k_trsv_stage<3, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
         }
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));

@@ -139,6 +139,7 @@ struct TriDev {
     const StageRec *recs;       // entry records, contiguous per task in position order
     const StageMeta *meta;      // per position (padded to nchunks * stage_ch)
     const double *ddiag;        // per position: {diag, RN(1/diag)} (staged solve's exact division)
+    long long *prof;            // optional per-phase cycle counters (RSB_TRSV_PROFILE), else null
 };
 
 // ---------------------------------------------------------------------------
@@ -177,10 +178,11 @@ struct TriSched {
     int64_t nrecs = 0;
     StageMeta *meta = nullptr;
     double *ddiag = nullptr;
+    long long *prof = nullptr;  // 8 counters, allocated when RSB_TRSV_PROFILE is set
     TriDev view() const {
         return TriDev{n,       mode,       task_row, slice_off,  ecol, eval, diag,   ticket,
                       has_far, (int32_t)nlevels,     level_ptr, stage_ch, stage_emax, nchunks,
-                      chunk_roff, bpos,    recs,     meta,       ddiag};
+                      chunk_roff, bpos,    recs,     meta,       ddiag, prof};
     }
 };
 

@@ -1,9 +1,9 @@
-"""Per-phase cycle breakdown of the staged single-CTA triangular solve, thread 0
-(experiment mode 3: the kernel writes clock64 totals into x[0..4])."""
-import json, os, sys
+"""Per-phase cycle breakdown of the staged triangular solve on config 1, thread 0
+(RSB_TRSV_PROFILE=1 makes the kernel accumulate clock64 phases into a side buffer)."""
+import ctypes, json, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["RSB_TRSV_EXPERIMENT"] = "3"
+os.environ["RSB_TRSV_PROFILE"] = "1"
 import paper_2603_28642_b200 as P
 from paper_2603_28642_b200 import _lib as L
 from paper_2603_28642_b200 import workloads as W
@@ -13,11 +13,14 @@ S, _ = P.column_scale(A)
 f = P.ilup_factorize(S, P.IlupParams(p=10, tau=0.0, mu=1.0))
 ctx = get_context(); n = f.U.ncols
 b = DeviceBuffer(ctx, n); b.upload(np.random.default_rng(0).standard_normal(n)); x = DeviceBuffer(ctx, n)
+L.lib().rsb_trsv_profile.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)]
 out = {}
 for name, M, kind in (("L1", f.L1, L.TRI_LOWER_UNIT), ("L1T", f.L1, L.TRI_LOWER_T_UNIT), ("U", f.U, L.TRI_UPPER)):
     dm = DeviceMatrix(M, ctx)
     for _ in range(3):
         L.check(L.lib().rsb_trsv(dm.h, kind, b.ptr, x.ptr, L.RSB_DEVICE))
-    v = x.download()[:5]
-    out[name] = {k: round(v[i] / v[4], 1) for i, k in enumerate(["issue", "wait", "task", "barrier"])}
+    c = (ctypes.c_longlong * 8)()
+    L.check(L.lib().rsb_trsv_profile(dm.h, kind, c))
+    nl = c[5]
+    out[name] = {k: round(c[i] / nl, 1) for i, k in [(0, "control+issue"), (6, "mbar_wait"), (1, "header"), (2, "chain"), (3, "div+store"), (4, "barrier+loop")]}
 print(json.dumps(out))
