@@ -360,6 +360,12 @@ __device__ __forceinline__ double ld_relaxed(const double *p) {
 // only waits on blocks already resident or done.  Warp-synchronous polling:
 // lanes never spin divergently; every round each pending lane checks all its
 // dependencies, the ready ones compute and publish, and the warp reconverges.
+// tasks longer than kPre (rare): out of line, keeps the fast path's registers low
+template <int MODE>
+__device__ __noinline__ double long_task_value(const TriDev &T, const Task &k, const double *x) {
+    return task_value<MODE>(T, k, [&](int j) { return ld_relaxed(x + j); });
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const double *c, double *x,
                                                     Gate g) {
@@ -373,9 +379,40 @@ __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const dou
     if (pending) load_task<MODE>(T, t, a, c, k);
     auto ready = [&](int j) { return __double_as_longlong(ld_relaxed(x + j)) != (long long)kSentinel; };
     while (__any_sync(0xffffffffu, pending)) {
-        if (pending && task_ready(T, k, ready)) {
-            publish(x + k.row, task_value<MODE>(T, k, [&](int j) { return ld_relaxed(x + j); }));
-            pending = false;
+        if (pending) {
+            if (k.len <= kPre) {
+                // one L2 round trip per poll: the polled values are the operands
+                double xv[kPre];
+                bool ok = true;
+#pragma unroll
+                for (int q = 0; q < kPre; ++q) {
+                    xv[q] = 0.0;
+                    if (q < k.len) {
+                        xv[q] = ld_relaxed(x + k.cols[q]);
+                        ok &= __double_as_longlong(xv[q]) != (long long)kSentinel;
+                    }
+                }
+                if (ok) {
+                    double acc = k.acc;
+                    if (!(MODE & 1)) {
+#pragma unroll
+                        for (int q = 0; q < kPre; ++q)
+                            if (q < k.len && xv[q] != 0.0) acc = __dsub_rn(acc, __dmul_rn(k.vals[q], xv[q]));
+                    } else if (k.len > 0) {
+                        double dot = 0.0;
+#pragma unroll
+                        for (int q = 0; q < kPre; ++q)
+                            if (q < k.len) dot = fma(k.vals[q], xv[q], dot);
+                        acc = __dsub_rn(acc, dot);
+                    }
+                    if (MODE & 2) acc = __ddiv_rn(acc, k.d);
+                    publish(x + k.row, acc);
+                    pending = false;
+                }
+            } else if (task_ready(T, k, ready)) {
+                publish(x + k.row, long_task_value<MODE>(T, k, x));
+                pending = false;
+            }
         }
         __syncwarp();
     }

@@ -24,13 +24,18 @@ def main():
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--mu", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--n", type=int, default=1_000_000)
     args = ap.parse_args()
     import paper_2603_28642_b200 as P
     from paper_2603_28642_b200 import _lib as L
     from paper_2603_28642_b200 import workloads as W
     from paper_2603_28642_b200.device import DeviceBuffer, DeviceMatrix, get_context
 
-    A, _ = W.config1(seed=1, g=args.grid)
+    if args.config == 4:
+        A, _ = W.config4(seed=4, n=args.n, nrhs=1)
+    else:
+        A, _ = W.config1(seed=1, g=args.grid)
     S, _ = P.column_scale(A)
     f = P.ilup_factorize(S, P.IlupParams(p=10, tau=0.0, mu=args.mu))
     ctx = get_context()
