@@ -156,3 +156,36 @@ def test_stagnation_visible_in_gradient_norm():
     _, rep = P.pcgls(S, b, pre, P.CglsConfig(norm_A=na))
     _, orep = O.pcgls(S, b, O.OraclePreconditioner.from_reference(pre), na)
     assert rep.to_dict() == orep
+
+
+def test_row_partitioned_device_backend_single_rank_bitwise():
+    """The row-partitioned host loop on the device backend (C-ABI kernels on
+    torch CUDA tensors) with one rank equals the device pcgls bit for bit."""
+    from paper_2603_28642_b200 import distributed as D
+    from paper_2603_28642_b200 import workloads as W
+    from paper_2603_28642_b200.device import default_device
+
+    class One:
+        rank, world = 0, 1
+
+        def allreduce_(self, t):
+            return t
+
+        def allreduce_scalar(self, v):
+            return v
+
+        def allgather_cat(self, t, sizes):
+            return t
+
+    A, b = W.config0(seed=11, m=600, n=400)
+    S, _ = P.column_scale(A)
+    na = P.power_method_norm2(S, 100, 11)
+    f = P.ilup_factorize(S, P.IlupParams(p=10, tau=1e-3, mu=1.0))
+    pre = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG)
+    cfg = P.CglsConfig(norm_A=na, delta=1e-8, max_iters=50)
+    x, rep = P.pcgls(S, b, pre, cfg)
+    xd, repd = D.pcgls_row_partitioned(S, b, pre, cfg, One(),
+                                       lambda Al, pr: D.DeviceBackend(Al, pr, default_device()))
+    assert np.array_equal(xd, x)
+    assert repd.its == rep.its and repd.ratio_pt_history == rep.ratio_pt_history
+    assert repd.residual_norm_final == rep.residual_norm_final
