@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-tol", action="store_true", help="skip the time-to-tolerance run")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--batch", type=int, default=8,
+                    help="also time this many concurrent RHS per GPU through pcgls_batch (0: skip)")
     ap.add_argument("--partition", default="replicas", choices=["replicas", "rows"],
                     help="N>1: replicas (one RHS per GPU, weak) or rows (one RHS, A row-partitioned, "
                          "NCCL allreduce of A^T r, strong)")
@@ -351,6 +353,22 @@ def run_b200(args):
     e2e_s = barrier_max(time.perf_counter() - t0)
     e2e = world * rep.its / e2e_s if not rep.converged else world * K / e2e_s
 
+    # ---- several independent RHS per GPU, solved concurrently
+    batch = None
+    if args.batch > 1:
+        rng = np.random.default_rng(77 + rank)
+        Bm = np.stack([b] + [b + 1e-3 * rng.standard_normal(len(b)) for _ in range(args.batch - 1)])
+        P.pcgls_batch(S, Bm, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
+        barrier()
+        t0 = time.perf_counter()
+        _, breps = P.pcgls_batch(S, Bm, pre, e2e_cfg)
+        b_s = barrier_max(time.perf_counter() - t0)
+        its = sum(K if r.converged else r.its for r in breps)
+        batch = {"rhs_per_gpu": args.batch, "value": world * its / b_s, "unit": "RHS-iter/s",
+                 "seconds": b_s,
+                 "call": f"pcgls_batch(A, B[{args.batch} x m] host, pre, CglsConfig(delta=1e-300, "
+                         f"max_iters={K})): one stream + workspace per RHS, shared A and factors"}
+
     # ---- time to tolerance (config delta), device path, reported alongside
     tol = None
     if not args.no_tol:
@@ -418,6 +436,7 @@ def run_b200(args):
                 "seconds": e2e_s},
         "gpu_launches": int(K * kpi[0]),
         "clocks": clocks.summary(),
+        "rhs_batch": batch,
         "time_to_tol": tol,
         "setup": {**times, "generate_s": t_gen},
         "tri_launches_timed": ntri,

@@ -159,6 +159,11 @@ typedef struct {
 /* A solver owns the iteration workspace for one (A, pre) pair and the
  * captured CUDA graph of one iteration.  pre may be NULL (plain CGLS). */
 int rsb_solver_create(rsb_mat *A, rsb_pre *pre, rsb_solver **out);
+/* the same, running on ctx's stream (same device as A and pre).  A and pre
+ * are read-only during a solve, so solvers on different contexts may share
+ * them and run concurrently: the batch of independent right-hand sides of
+ * config 4. */
+int rsb_solver_create_on(rsb_ctx *ctx, rsb_mat *A, rsb_pre *pre, rsb_solver **out);
 int rsb_solver_destroy(rsb_solver *S);
 /* x = 0, r = b, z = A^T r, h, rho, p (sv.py:147-200).  *status: 0 running,
  * 4 = z.z == 0 at the start (x = 0 is stationary, sv.py:184-196). */
@@ -182,6 +187,13 @@ int rsb_l2_flush(rsb_ctx *ctx);
 /* whole solve in one call: start + iterate + finish + get_x */
 int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, double *x,
               rsb_report *rep, double *history, int64_t history_cap);
+/* count independent solves, S[i] on b[i] -> x[i], reps[i] and
+ * history[i*history_cap ...], advanced together so they overlap on the
+ * device.  Solvers must be on distinct contexts.  Each result equals
+ * rsb_pcgls on that solver alone, bit for bit. */
+int rsb_pcgls_many(int count, rsb_solver *const *S, const double *const *b, int where,
+                   const rsb_cgls_cfg *cfg, double *const *x, rsb_report *reps, double *history,
+                   int64_t history_cap);
 
 /* ---- host setup (stays on the CPU; timed separately) -------------------- */
 /* ilup_factorize (il.py:211-368), bit-identical factors.  Inputs: scaled A

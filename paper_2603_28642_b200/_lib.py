@@ -78,12 +78,15 @@ _SIGS = {
     "rsb_pre_y_apply_transpose": [vp, vp, vp, ctypes.c_int],
     "rsb_pre_s_matvec": [vp, vp, vp, ctypes.c_int],
     "rsb_solver_create": [vp, vp, ctypes.POINTER(vp)],
+    "rsb_solver_create_on": [vp, vp, vp, ctypes.POINTER(vp)],
     "rsb_solver_destroy": [vp],
     "rsb_solver_start": [vp, vp, ctypes.c_int, ctypes.POINTER(CglsCfgC), ctypes.POINTER(ctypes.c_int)],
     "rsb_solver_iterate": [vp, i64, i64p, ctypes.POINTER(ctypes.c_int)],
     "rsb_solver_get_x": [vp, vp, ctypes.c_int],
     "rsb_solver_finish": [vp, ctypes.POINTER(ReportC), vp, i64],
     "rsb_pcgls": [vp, vp, ctypes.c_int, ctypes.POINTER(CglsCfgC), vp, ctypes.POINTER(ReportC), vp, i64],
+    "rsb_pcgls_many": [ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(CglsCfgC),
+                       ctypes.POINTER(vp), ctypes.POINTER(ReportC), vp, i64],
     "rsb_solver_bench": [vp, i64, ctypes.c_int, f64p, f64p, i64p, i64p, ctypes.POINTER(ctypes.c_int)],
     "rsb_l2_flush": [vp],
     "rsb_ilup_factorize": [i64, i64, vp, vp, vp, i64, f64, f64, f64, ctypes.POINTER(vp)],

@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const dou
                                                     Gate g) {
     if (gated(g)) return;
     __shared__ int s_blk;
-    if (threadIdx.x == 0) s_blk = (int)(atomicAdd(T.ticket, 1ull) % gridDim.x);
+    if (threadIdx.x == 0) s_blk = (int)atomicAdd(T.ticket, 1ull);
     __syncthreads();
     const int t = s_blk * kTriBlock + threadIdx.x;
     bool pending = t < T.n;
@@ -892,16 +892,25 @@ int launch_fill(rsb_ctx *ctx, double *x, int64_t n, unsigned long long bits, Gat
     return post_launch(ctx);
 }
 
-int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g) {
+int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g,
+                const TriWs *ws) {
     if (T.n == 0) return RSB_OK;
     const bool trace = ctx->tracing && ctx->trace_n + 2 <= 64;
     if (trace)
         RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
-    const TriDev v = T.view();
+    TriDev v = T.view();
+    if (ws) {
+        if (T.single_cta && ws->cap < T.padded_n) {
+            set_error("triangular-solve scratch too small (%lld < %lld)", (long long)ws->cap, (long long)T.padded_n);
+            return RSB_ESTATE;
+        }
+        v.bpos = ws->bpos;
+        v.ticket = ws->ticket;
+    }
     if (T.single_cta) {
         const size_t smem = (size_t)stage_smem_bytes(T.stage_ch, T.stage_emax, T.diag != nullptr, T.nlevels, T.nchunks);
         k_gather_pos<<<grid_stride(T.padded_n), kBlock, 0, ctx->stream>>>(T.n, T.padded_n, T.task_row, a, c,
-                                                                          T.bpos, g);
+                                                                          v.bpos, g);
         RSB_TRY(post_launch(ctx));
         const int sel = T.mode + (T.has_far ? 4 : 0);
         switch (sel) {
@@ -916,6 +925,8 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         }
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
+        // blocks number themselves in start order from this counter
+        RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
         const int grid = grid_for(T.n, kTriBlock);
         switch (T.mode) {
             case 0: k_trsv<0><<<grid, kTriBlock, 0, ctx->stream>>>(v, a, c, x, g); break;
@@ -928,6 +939,20 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
     if (trace)
         RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
     return RSB_OK;
+}
+
+int tri_ws_alloc(rsb_ctx *ctx, TriWs &w, int64_t cap) {
+    RSB_TRY(dev_alloc(ctx, (void **)&w.bpos, (size_t)std::max<int64_t>(cap, 1) * sizeof(double)));
+    w.cap = cap;
+    RSB_TRY(dev_alloc(ctx, (void **)&w.ticket, sizeof(unsigned long long)));
+    RSB_TRY_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned long long), ctx->stream));
+    return RSB_OK;
+}
+
+void tri_ws_free(rsb_ctx *ctx, TriWs &w) {
+    if (w.bpos) dev_free(ctx, w.bpos, (size_t)std::max<int64_t>(w.cap, 1) * sizeof(double));
+    if (w.ticket) dev_free(ctx, w.ticket, sizeof(unsigned long long));
+    w = TriWs{};
 }
 
 int prepare_trsv_cta(int64_t smem_bytes) {

@@ -264,6 +264,18 @@ int prepare_chol(int64_t s);
 // one-time kernel attribute setup at context creation (dynamic shared memory)
 int prepare_kernels();
 
+// Per-stream scratch of triangular solves: the gathered right-hand side of the
+// staged kernel and the block ticket of the grid kernel.  Owned by whoever
+// launches (a preconditioner's workspace, a solver), never by the immutable
+// schedule, so solves on different streams can share one schedule.
+struct TriWs {
+    double *bpos = nullptr;
+    int64_t cap = 0;
+    unsigned long long *ticket = nullptr;
+};
+int tri_ws_alloc(rsb_ctx *ctx, TriWs &w, int64_t cap);
+void tri_ws_free(rsb_ctx *ctx, TriWs &w);
+
 // triangular-solve analysis (analysis.cpp)
 int tri_analyse(rsb_mat *T, int kind, TriSched **out);
 void tri_free(rsb_ctx *ctx, TriSched *s);
@@ -278,7 +290,9 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
 // z(j) = acc | e(j) + acc, acc = p0 + pairwise(p1..), p = vals * y[rows] (sc.py:231-234)
 int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g);
 // triangular solve of a schedule: x(row) = solve with rhs(row) = a(row) [+ c[row]]
-int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g);
+// (ws: the launcher's scratch; nullptr uses the schedule's own, for standalone calls)
+int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g,
+                const TriWs *ws = nullptr);
 // out[0] = a.b (sqrt_out: sqrt(a.b)) in the context's dot order; need: optional
 // flag that must be nonzero for the dot to run
 int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,

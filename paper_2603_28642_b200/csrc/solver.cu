@@ -245,6 +245,22 @@ using namespace rsb;
 // ---------------------------------------------------------------------------
 // preconditioner (pc.py:106-186)
 // ---------------------------------------------------------------------------
+// Mutable state of one preconditioner application stream: vectors, the inner
+// CG control block and the triangular-solve scratch.  The preconditioner
+// itself is immutable (pc.py:111-113); every user of it -- its own standalone
+// entry points and every solver -- owns an ApplyWs, so independent solves can
+// run concurrently on different streams.
+struct ApplyWs {
+    rsb_ctx *ctx = nullptr;
+    int64_t n = 0, s = 0;
+    double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *v = nullptr;  // n
+    double *u = nullptr, *w = nullptr;                                  // s
+    double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;            // s
+    double *cg_a = nullptr, *cg_b = nullptr, *cg_c = nullptr;            // n
+    CgState *cg = nullptr;
+    TriWs tri;
+};
+
 struct rsb_pre {
     rsb_ctx *ctx = nullptr;
     int64_t m = 0, n = 0, s = 0;
@@ -253,95 +269,113 @@ struct rsb_pre {
     rsb_mat *L1 = nullptr, *L2 = nullptr, *U = nullptr, *Y = nullptr;
     TriSched *tL1 = nullptr, *tL1T = nullptr, *tU = nullptr;
     double *S = nullptr;  // s x s lower factor, column-major
-    // workspace
-    double *t1 = nullptr, *t2 = nullptr, *t3 = nullptr, *v = nullptr;  // n
-    double *u = nullptr, *w = nullptr;                                  // s
-    double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;            // s
-    double *cg_a = nullptr, *cg_b = nullptr, *cg_c = nullptr;            // n
-    CgState *cg = nullptr;
+    ApplyWs ws;           // for the standalone entry points (pc.py:135-186)
 };
 
 namespace {
 
-// q = S p = p + L2 L1^{-1} L1^{-T} L2^T p  (s_matvec_implicit, pc.py:149-154)
-int enqueue_s_matvec(rsb_pre *P, const double *p, double *q, Gate g) {
-    rsb_ctx *ctx = P->ctx;
-    RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{p, nullptr, 0}, P->cg_a, EPI_STORE, VecIn{}, g));
-    RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->cg_a, nullptr, 0}, nullptr, P->cg_b, g));
-    RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{P->cg_b, nullptr, 0}, nullptr, P->cg_c, g));
-    RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->cg_c, nullptr, 0}, q, EPI_ADD, VecIn{p, nullptr, 0}, g));
+int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W) {
+    W.ctx = ctx;
+    W.n = P->n;
+    W.s = P->s;
+    const size_t n8 = P->n * sizeof(double), s8 = P->s * sizeof(double);
+    for (double **q : {&W.t1, &W.t2, &W.t3, &W.v, &W.cg_a, &W.cg_b, &W.cg_c}) RSB_TRY(dev_alloc(ctx, (void **)q, n8));
+    for (double **q : {&W.u, &W.w, &W.cg_r, &W.cg_p, &W.cg_q}) RSB_TRY(dev_alloc(ctx, (void **)q, s8));
+    RSB_TRY(dev_alloc(ctx, (void **)&W.cg, sizeof(CgState)));
+    RSB_TRY_CUDA(cudaMemsetAsync(W.cg, 0, sizeof(CgState), ctx->stream));
+    int64_t cap = 0;
+    for (const TriSched *T : {P->tL1, P->tL1T, P->tU})
+        if (T) cap = std::max(cap, T->padded_n);
+    RSB_TRY(tri_ws_alloc(ctx, W.tri, cap));
     return RSB_OK;
 }
 
-// w = _cg_fixed_steps(S, u, k)  (pc.py:284-310); returns the buffer holding w
-int enqueue_cg(rsb_pre *P, const double *u, Gate outer) {
-    rsb_ctx *ctx = P->ctx;
+void ws_free(ApplyWs &W) {
+    if (!W.ctx) return;
+    const size_t n8 = W.n * sizeof(double), s8 = W.s * sizeof(double);
+    for (double *q : {W.t1, W.t2, W.t3, W.v, W.cg_a, W.cg_b, W.cg_c}) dev_free(W.ctx, q, n8);
+    for (double *q : {W.u, W.w, W.cg_r, W.cg_p, W.cg_q}) dev_free(W.ctx, q, s8);
+    dev_free(W.ctx, W.cg, sizeof(CgState));
+    tri_ws_free(W.ctx, W.tri);
+    W.ctx = nullptr;
+}
+
+// q = S p = p + L2 L1^{-1} L1^{-T} L2^T p  (s_matvec_implicit, pc.py:149-154)
+int enqueue_s_matvec(rsb_pre *P, ApplyWs &W, const double *p, double *q, Gate g) {
+    rsb_ctx *ctx = W.ctx;
+    RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{p, nullptr, 0}, W.cg_a, EPI_STORE, VecIn{}, g));
+    RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{W.cg_a, nullptr, 0}, nullptr, W.cg_b, g, &W.tri));
+    RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{W.cg_b, nullptr, 0}, nullptr, W.cg_c, g, &W.tri));
+    RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{W.cg_c, nullptr, 0}, q, EPI_ADD, VecIn{p, nullptr, 0}, g));
+    return RSB_OK;
+}
+
+// w = _cg_fixed_steps(S, u, k)  (pc.py:284-310), result in W.w
+int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
+    rsb_ctx *ctx = W.ctx;
     const int64_t s = P->s;
-    CgState *cg = P->cg;
-    k_cg_init<<<small_grid(s), 256, 0, ctx->stream>>>(P->w, P->cg_r, P->cg_p, u, s, outer);
+    CgState *cg = W.cg;
+    k_cg_init<<<small_grid(s), 256, 0, ctx->stream>>>(W.w, W.cg_r, W.cg_p, u, s, outer);
     RSB_TRY(chk(ctx));
-    RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_r, nullptr, 0}, VecIn{P->cg_r, nullptr, 0}, &cg->rho, 0, outer, nullptr));
+    RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_r, nullptr, 0}, VecIn{W.cg_r, nullptr, 0}, &cg->rho, 0, outer, nullptr));
     k_cg_start<<<1, 1, 0, ctx->stream>>>(cg, outer);
     RSB_TRY(chk(ctx));
     Gate g{outer.a, &cg->stop};
     for (int it = 0; it < P->cg_iters; ++it) {
-        RSB_TRY(enqueue_s_matvec(P, P->cg_p, P->cg_q, g));
-        RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_p, nullptr, 0}, VecIn{P->cg_q, nullptr, 0}, &cg->pq, 0, g, nullptr));
+        RSB_TRY(enqueue_s_matvec(P, W, W.cg_p, W.cg_q, g));
+        RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_p, nullptr, 0}, VecIn{W.cg_q, nullptr, 0}, &cg->pq, 0, g, nullptr));
         k_cg_alpha<<<1, 1, 0, ctx->stream>>>(cg, g);
         RSB_TRY(chk(ctx));
-        RSB_TRY(launch_axpy(ctx, P->w, P->cg_p, &cg->alpha, +1, s, g));
-        RSB_TRY(launch_axpy(ctx, P->cg_r, P->cg_q, &cg->alpha, -1, s, g));
-        RSB_TRY(launch_dot(ctx, s, VecIn{P->cg_r, nullptr, 0}, VecIn{P->cg_r, nullptr, 0}, &cg->rho_new, 0, g, nullptr));
+        RSB_TRY(launch_axpy(ctx, W.w, W.cg_p, &cg->alpha, +1, s, g));
+        RSB_TRY(launch_axpy(ctx, W.cg_r, W.cg_q, &cg->alpha, -1, s, g));
+        RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_r, nullptr, 0}, VecIn{W.cg_r, nullptr, 0}, &cg->rho_new, 0, g, nullptr));
         k_cg_beta<<<1, 1, 0, ctx->stream>>>(cg, g);
         RSB_TRY(chk(ctx));
-        RSB_TRY(launch_xpby(ctx, P->cg_p, P->cg_r, &cg->beta, nullptr, s, g));
+        RSB_TRY(launch_xpby(ctx, W.cg_p, W.cg_r, &cg->beta, nullptr, s, g));
     }
     return RSB_OK;
 }
 
 // h = apply(r1, r2)  (pc.py:175-186)
-int enqueue_apply(rsb_pre *P, VecIn r1, VecIn r2, double *h, Gate g) {
-    rsb_ctx *ctx = P->ctx;
+int enqueue_apply(rsb_pre *P, ApplyWs &W, VecIn r1, VecIn r2, double *h, Gate g) {
+    rsb_ctx *ctx = W.ctx;
     if (P->s > 0) {
         // u = r2 - Y r1
         if (P->y_mode == RSB_Y_EXPLICIT) {
-            RSB_TRY(launch_spmv(ctx, P->Y->csr(), r1, P->u, EPI_SUB_FROM, r2, g));
+            RSB_TRY(launch_spmv(ctx, P->Y->csr(), r1, W.u, EPI_SUB_FROM, r2, g));
         } else {
-            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, P->t1, g));
-            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->t1, nullptr, 0}, P->u, EPI_SUB_FROM, r2, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, W.t1, g, &W.tri));
+            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{W.t1, nullptr, 0}, W.u, EPI_SUB_FROM, r2, g));
         }
         // w = solve_S(u)
-        const double *w = P->w;
+        const double *w = W.w;
         if (P->s_mode == RSB_S_DENSE) {
-            RSB_TRY(launch_chol_solve(ctx, P->S, P->s, P->u, P->w, g));
+            RSB_TRY(launch_chol_solve(ctx, P->S, P->s, W.u, W.w, g));
         } else if (P->s_mode == RSB_S_IDENTITY) {
-            w = P->u;
+            w = W.u;
         } else {
-            RSB_TRY(enqueue_cg(P, P->u, g));
+            RSB_TRY(enqueue_cg(P, W, W.u, g));
         }
         // y = r1 + Y^T w ; v = L1^{-1} y
         if (P->y_mode == RSB_Y_EXPLICIT) {
-            RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{w, nullptr, 0}, P->t3, EPI_ADD, r1, g));
-            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{P->t3, nullptr, 0}, nullptr, P->v, g));
+            RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{w, nullptr, 0}, W.t3, EPI_ADD, r1, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{W.t3, nullptr, 0}, nullptr, W.v, g, &W.tri));
         } else {
-            RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{w, nullptr, 0}, P->t2, EPI_STORE, VecIn{}, g));
-            RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->t2, nullptr, 0}, nullptr, P->t3, g));
-            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, P->t3, P->v, g));
+            RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{w, nullptr, 0}, W.t2, EPI_STORE, VecIn{}, g));
+            RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{W.t2, nullptr, 0}, nullptr, W.t3, g, &W.tri));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, W.t3, W.v, g, &W.tri));
         }
     } else {
-        RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, P->v, g));
+        RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, W.v, g, &W.tri));
     }
-    return launch_trsv(ctx, *P->tU, VecIn{P->v, nullptr, 0}, nullptr, h, g);
+    return launch_trsv(ctx, *P->tU, VecIn{W.v, nullptr, 0}, nullptr, h, g, &W.tri);
 }
 
 void pre_free(rsb_pre *P) {
     rsb_ctx *ctx = P->ctx;
-    const size_t n8 = P->n * sizeof(double), s8 = P->s * sizeof(double);
     dev_free(ctx, P->perm, P->m * sizeof(int32_t));
     if (P->S) dev_free(ctx, P->S, P->s * P->s * sizeof(double));
-    for (double *q : {P->t1, P->t2, P->t3, P->v, P->cg_a, P->cg_b, P->cg_c}) dev_free(ctx, q, n8);
-    for (double *q : {P->u, P->w, P->cg_r, P->cg_p, P->cg_q}) dev_free(ctx, q, s8);
-    dev_free(ctx, P->cg, sizeof(CgState));
+    ws_free(P->ws);
     delete P;
 }
 
@@ -351,9 +385,10 @@ void pre_free(rsb_pre *P) {
 // solver (sv.py:120-268)
 // ---------------------------------------------------------------------------
 struct rsb_solver {
-    rsb_ctx *ctx = nullptr;
+    rsb_ctx *ctx = nullptr;  // the solver's stream; may differ from the matrices' (same device)
     rsb_mat *A = nullptr;
     rsb_pre *pre = nullptr;
+    ApplyWs ws;              // this solver's preconditioner workspace
     int64_t m = 0, n = 0;
     double *b = nullptr, *x = nullptr, *r = nullptr, *q = nullptr, *fr = nullptr;  // m: b, r, q, fr
     double *z = nullptr, *h = nullptr, *p = nullptr, *g = nullptr;                 // n
@@ -379,7 +414,7 @@ namespace {
 int enqueue_precondition(rsb_solver *S, Gate g) {
     if (S->pre) {
         const rsb_pre *P = S->pre;
-        return enqueue_apply(S->pre, VecIn{S->r, P->perm, 0}, VecIn{S->r, P->perm, S->n}, S->h, g);
+        return enqueue_apply(S->pre, S->ws, VecIn{S->r, P->perm, 0}, VecIn{S->r, P->perm, S->n}, S->h, g);
     }
     return launch_copy(S->ctx, S->h, VecIn{S->z, nullptr, 0}, S->n, g);  // h = A^T r (sv.py:166-167)
 }
@@ -489,6 +524,7 @@ void solver_free(rsb_solver *S) {
     dev_free(ctx, S->sigmas, S->cap * sizeof(double));
     dev_free(ctx, S->x_norms, (S->cap + 1) * sizeof(double));
     dev_free(ctx, S->history, (S->cap + S->d + 1) * sizeof(double));
+    ws_free(S->ws);
     delete S;
 }
 
@@ -553,17 +589,14 @@ int rsb_pre_create(rsb_ctx *ctx, int64_t m, int64_t n, const int64_t *perm, rsb_
     }
     PTRY(get_tri(L1, RSB_TRI_LOWER_UNIT, &P->tL1));
     PTRY(get_tri(U, RSB_TRI_UPPER, &P->tU));
-    if (s > 0 && (y_mode == RSB_Y_IMPLICIT || s_mode == RSB_S_CG)) PTRY(get_tri(L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
+    if (s > 0) PTRY(get_tri(L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
     PTRY(dev_upload(ctx, &P->perm, pm.data(), pm.size()));
     if (s_mode == RSB_S_DENSE && s > 0) {
         PTRY(dev_upload(ctx, &P->S, S_factor, (size_t)(s * s)));
         PTRY(prepare_chol(s));
     }
-    for (double **q : {&P->t1, &P->t2, &P->t3, &P->v, &P->cg_a, &P->cg_b, &P->cg_c}) PTRY(dev_alloc(ctx, (void **)q, n8));
-    for (double **q : {&P->u, &P->w, &P->cg_r, &P->cg_p, &P->cg_q}) PTRY(dev_alloc(ctx, (void **)q, s8));
-    PTRY(dev_alloc(ctx, (void **)&P->cg, sizeof(CgState)));
+    PTRY(ws_alloc(ctx, P, P->ws));
 #undef PTRY
-    RSB_TRY_CUDA(cudaMemsetAsync(P->cg, 0, sizeof(CgState), ctx->stream));
     RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = P;
     return RSB_OK;
@@ -583,7 +616,7 @@ int rsb_pre_apply(rsb_pre *P, const double *r1, const double *r2, double *h, int
     RSB_TRY(stage_in(ctx, r1, P->n, where, s1));
     RSB_TRY(stage_in(ctx, r2, P->s, where, s2));
     RSB_TRY(stage_out(ctx, h, P->n, where, sh));
-    RSB_TRY(enqueue_apply(P, VecIn{s1.d, nullptr, 0}, VecIn{s2.d, nullptr, 0}, sh.d, Gate{}));
+    RSB_TRY(enqueue_apply(P, P->ws, VecIn{s1.d, nullptr, 0}, VecIn{s2.d, nullptr, 0}, sh.d, Gate{}));
     return finish_out(ctx, h, P->n, where, sh);
 }
 
@@ -597,8 +630,8 @@ int rsb_pre_y_apply(rsb_pre *P, const double *r1, double *out, int where) {
         if (P->y_mode == RSB_Y_EXPLICIT) {
             RSB_TRY(launch_spmv(ctx, P->Y->csr(), VecIn{s1.d, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
         } else {
-            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{s1.d, nullptr, 0}, nullptr, P->t1, Gate{}));
-            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->t1, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
+            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{s1.d, nullptr, 0}, nullptr, P->ws.t1, Gate{}, &P->ws.tri));
+            RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{P->ws.t1, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
         }
     }
     return finish_out(ctx, out, P->s, where, so);
@@ -613,9 +646,8 @@ int rsb_pre_y_apply_transpose(rsb_pre *P, const double *w, double *out, int wher
     if (P->y_mode == RSB_Y_EXPLICIT) {
         RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{sw.d, nullptr, 0}, so.d, EPI_STORE, VecIn{}, Gate{}));
     } else {
-        if (!P->tL1T) RSB_TRY(get_tri(P->L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
-        RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{sw.d, nullptr, 0}, P->t2, EPI_STORE, VecIn{}, Gate{}));
-        RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->t2, nullptr, 0}, nullptr, so.d, Gate{}));
+        RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{sw.d, nullptr, 0}, P->ws.t2, EPI_STORE, VecIn{}, Gate{}));
+        RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{P->ws.t2, nullptr, 0}, nullptr, so.d, Gate{}, &P->ws.tri));
     }
     return finish_out(ctx, out, P->n, where, so);
 }
@@ -627,24 +659,29 @@ int rsb_pre_s_matvec(rsb_pre *P, const double *v, double *out, int where) {
     RSB_TRY(stage_in(ctx, v, P->s, where, sv));
     RSB_TRY(stage_out(ctx, out, P->s, where, so));
     if (P->s > 0) {
-        if (!P->tL1T) RSB_TRY(get_tri(P->L1, RSB_TRI_LOWER_T_UNIT, &P->tL1T));
-        RSB_TRY(enqueue_s_matvec(P, sv.d, so.d, Gate{}));
+        RSB_TRY(enqueue_s_matvec(P, P->ws, sv.d, so.d, Gate{}));
     }
     return finish_out(ctx, out, P->s, where, so);
 }
 
 int rsb_solver_create(rsb_mat *A, rsb_pre *pre, rsb_solver **out) {
+    return rsb_solver_create_on(A->ctx, A, pre, out);
+}
+
+int rsb_solver_create_on(rsb_ctx *ctx, rsb_mat *A, rsb_pre *pre, rsb_solver **out) {
     *out = nullptr;
-    rsb_ctx *ctx = A->ctx;
     if (pre && (pre->m != A->nrows || pre->n != A->ncols)) {
         set_error("preconditioner does not match the matrix");
         return RSB_EINVAL;
     }
-    if (pre && pre->ctx != ctx) {
-        set_error("matrix and preconditioner belong to different contexts");
+    if (A->ctx->device != ctx->device || (pre && pre->ctx->device != ctx->device)) {
+        set_error("matrix, preconditioner and solver context must be on the same device");
         return RSB_EINVAL;
     }
     RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    // the shared matrices were uploaded on their own streams
+    RSB_TRY_CUDA(cudaStreamSynchronize(A->ctx->stream));
+    if (pre) RSB_TRY_CUDA(cudaStreamSynchronize(pre->ctx->stream));
     auto *S = new rsb_solver();
     S->ctx = ctx;
     S->A = A;
@@ -662,6 +699,8 @@ int rsb_solver_create(rsb_mat *A, rsb_pre *pre, rsb_solver **out) {
         set_error("pinned allocation failed");
         rc = RSB_ENOMEM;
     }
+    if (rc == RSB_OK && pre) rc = ws_alloc(ctx, pre, S->ws);
+    if (rc == RSB_OK) rc = cudaStreamSynchronize(ctx->stream) == cudaSuccess ? RSB_OK : RSB_ECUDA;
     if (rc != RSB_OK) {
         solver_free(S);
         return rc;
@@ -675,7 +714,13 @@ int rsb_solver_destroy(rsb_solver *S) {
     return RSB_OK;
 }
 
-int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, int *status) {
+}  // extern "C"
+
+namespace {
+
+// sv.py:152-200 enqueued on the solver's stream, ending with an async read of
+// the control block into the pinned mirror (no synchronisation)
+int start_enqueue(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg) {
     rsb_ctx *ctx = S->ctx;
     RSB_TRY_CUDA(cudaSetDevice(ctx->device));
     if (!(cfg->delta > 0.0) || cfg->estimator_delay < 1 || cfg->max_iters < 1) {
@@ -684,6 +729,7 @@ int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_c
     }
     RSB_TRY(ensure_capacity(S, cfg->max_iters, cfg->estimator_delay));
     S->cfg = *cfg;
+    S->started = false;
     const int64_t m = S->m, n = S->n;
     if (where == RSB_DEVICE) {
         RSB_TRY_CUDA(cudaMemcpyAsync(S->b, b, m * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -696,6 +742,9 @@ int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_c
     init.max_iters = cfg->max_iters;
     init.d = cfg->estimator_delay;
     init.ratio_raw = cfg->ratio_raw;
+    // the mirror may still be the source of an in-flight copy from a
+    // previous start on this stream
+    RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     *S->h_st = init;
     RSB_TRY_CUDA(cudaMemcpyAsync(S->st, S->h_st, sizeof(CglsState), cudaMemcpyHostToDevice, ctx->stream));
     CglsState *st = S->st;
@@ -715,7 +764,14 @@ int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_c
     k_start_rho<<<1, 1, 0, ctx->stream>>>(st, S->x_norms);
     RSB_TRY(chk(ctx));
     RSB_TRY(launch_copy(ctx, S->p, VecIn{S->h, nullptr, 0}, n, g));
-    RSB_TRY(read_state(S));
+    RSB_TRY_CUDA(cudaMemcpyAsync(S->h_st, S->st, sizeof(CglsState), cudaMemcpyDeviceToHost, ctx->stream));
+    return RSB_OK;
+}
+
+// after start_enqueue: wait for the control block and check it
+int start_complete(rsb_solver *S, int *status) {
+    RSB_TRY_CUDA(cudaSetDevice(S->ctx->device));
+    RSB_TRY_CUDA(cudaStreamSynchronize(S->ctx->stream));
     if (S->h_st->status == ST_ERROR) {
         set_error("zero denominator in stopping ratio");
         return RSB_EINVAL;
@@ -723,6 +779,25 @@ int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_c
     S->started = true;
     *status = S->h_st->status;
     return RSB_OK;
+}
+
+// enqueue up to nb iteration-graph replays and an async state read
+int iterate_enqueue(rsb_solver *S, int64_t nb) {
+    rsb_ctx *ctx = S->ctx;
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    for (int64_t i = 0; i < nb; ++i) RSB_TRY_CUDA(cudaGraphLaunch(S->exec, ctx->stream));
+    ctx->launches += nb * S->graph_kernels;
+    RSB_TRY_CUDA(cudaMemcpyAsync(S->h_st, S->st, sizeof(CglsState), cudaMemcpyDeviceToHost, ctx->stream));
+    return RSB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rsb_solver_start(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg, int *status) {
+    RSB_TRY(start_enqueue(S, b, where, cfg));
+    return start_complete(S, status);
 }
 
 int rsb_solver_iterate(rsb_solver *S, int64_t k, int64_t *iters_run, int *status) {
@@ -739,10 +814,9 @@ int rsb_solver_iterate(rsb_solver *S, int64_t k, int64_t *iters_run, int *status
     int64_t batch = 4;
     while (st == ST_RUN && done < k) {
         const int64_t nb = std::min(batch, k - done);
-        for (int64_t i = 0; i < nb; ++i) RSB_TRY_CUDA(cudaGraphLaunch(S->exec, ctx->stream));
-        ctx->launches += nb * S->graph_kernels;
+        RSB_TRY(iterate_enqueue(S, nb));
         done += nb;
-        RSB_TRY(read_state(S));
+        RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
         st = S->h_st->status;
         batch = std::min<int64_t>(batch * 2, 64);
     }
@@ -902,6 +976,56 @@ int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg
     }
     RSB_TRY(rsb_solver_finish(S, rep, history, history_cap));
     return rsb_solver_get_x(S, x, where);
+}
+
+// Independent solves on several solvers (one stream each, same device or
+// not), advanced together: every solver's graph batch is enqueued before the
+// host waits on any of them, so the solves overlap on the device.  Each
+// solver's arithmetic is exactly rsb_pcgls's.
+int rsb_pcgls_many(int count, rsb_solver *const *S, const double *const *b, int where, const rsb_cgls_cfg *cfg,
+                   double *const *x, rsb_report *reps, double *history, int64_t history_cap) {
+    if (count < 0) {
+        set_error("count must be >= 0");
+        return RSB_EINVAL;
+    }
+    for (int i = 0; i < count; ++i)
+        for (int j = 0; j < i; ++j)
+            if (S[i] == S[j] || S[i]->ctx == S[j]->ctx) {
+                set_error("rsb_pcgls_many needs distinct solvers on distinct contexts");
+                return RSB_EINVAL;
+            }
+    std::vector<int> st(count, ST_RUN);
+    for (int i = 0; i < count; ++i) RSB_TRY(start_enqueue(S[i], b[i], where, cfg));
+    for (int i = 0; i < count; ++i) RSB_TRY(start_complete(S[i], &st[i]));
+    std::vector<int64_t> done(count, 0);
+    int64_t batch = 4;
+    for (;;) {
+        bool any = false;
+        for (int i = 0; i < count; ++i) {
+            if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
+            RSB_TRY(iterate_enqueue(S[i], std::min(batch, cfg->max_iters - done[i])));
+            any = true;
+        }
+        if (!any) break;
+        for (int i = 0; i < count; ++i) {
+            if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
+            done[i] += std::min(batch, cfg->max_iters - done[i]);
+            RSB_TRY_CUDA(cudaSetDevice(S[i]->ctx->device));
+            RSB_TRY_CUDA(cudaStreamSynchronize(S[i]->ctx->stream));
+            st[i] = S[i]->h_st->status;
+            if (st[i] == ST_ERROR) {
+                set_error("zero denominator in stopping ratio");
+                return RSB_EINVAL;
+            }
+        }
+        batch = std::min<int64_t>(batch * 2, 64);
+    }
+    for (int i = 0; i < count; ++i) {
+        RSB_TRY(rsb_solver_finish(S[i], &reps[i], history ? history + i * history_cap : nullptr,
+                                  history ? history_cap : 0));
+        RSB_TRY(rsb_solver_get_x(S[i], x[i], where));
+    }
+    return RSB_OK;
 }
 
 // power_method_norm2 (sc.py:428-454); v0 drawn on the host

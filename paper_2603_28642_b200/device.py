@@ -207,6 +207,7 @@ def device_matrix(A, ctx: Context | None = None) -> DeviceMatrix:
 
 
 def clear_caches():
+    _batch_cache.clear()
     _mat_cache.clear()
     _pre_cache.clear()
     _solver_cache.clear()
@@ -302,11 +303,12 @@ def device_preconditioner(pre, ctx: Context | None = None) -> DevicePrecondition
 class DeviceSolver:
     """Workspace + captured iteration graph for pcgls on one (A, pre) pair."""
 
-    def __init__(self, dA: DeviceMatrix, dpre: DevicePreconditioner | None):
+    def __init__(self, dA: DeviceMatrix, dpre: DevicePreconditioner | None, ctx: Context | None = None):
         self.dA, self.dpre = dA, dpre
-        self.ctx = dA.ctx
+        self.ctx = dA.ctx if ctx is None else ctx
         h = ctypes.c_void_p()
-        L.check(L.lib().rsb_solver_create(dA.h, dpre.h if dpre is not None else None, ctypes.byref(h)))
+        L.check(L.lib().rsb_solver_create_on(self.ctx.h, dA.h, dpre.h if dpre is not None else None,
+                                             ctypes.byref(h)))
         self.h = h
 
     @staticmethod
@@ -354,4 +356,38 @@ def device_solver(dA: DeviceMatrix, dpre: DevicePreconditioner | None) -> Device
     _solver_cache[key] = s
     while len(_solver_cache) > 8:
         _solver_cache.popitem(last=False)
+    return s
+
+
+_stream_pool: dict[int, list[Context]] = {}
+
+
+def stream_contexts(k: int, device: int | None = None) -> list[Context]:
+    """k distinct contexts (streams) on one device for concurrent solves; the
+    first is the device's default context."""
+    dev = default_device() if device is None else device
+    with _ctx_lock:
+        pool = _stream_pool.setdefault(dev, [])
+    first = get_context(dev)
+    with _ctx_lock:
+        while len(pool) < k - 1:
+            pool.append(Context(dev))
+        return [first] + pool[: k - 1]
+
+
+_batch_cache: "collections.OrderedDict[tuple, list[DeviceSolver]]" = collections.OrderedDict()
+
+
+def device_solvers(dA: DeviceMatrix, dpre: DevicePreconditioner | None, k: int) -> list[DeviceSolver]:
+    """k solvers sharing dA and dpre, one per stream."""
+    key = (id(dA), id(dpre), k)
+    s = _batch_cache.get(key)
+    if s is not None and s[0].dA is dA and s[0].dpre is dpre:
+        _batch_cache.move_to_end(key)
+        return s
+    ctxs = stream_contexts(k, dA.ctx.device)
+    s = [device_solver(dA, dpre)] + [DeviceSolver(dA, dpre, c) for c in ctxs[1:]]
+    _batch_cache[key] = s
+    while len(_batch_cache) > 4:
+        _batch_cache.popitem(last=False)
     return s

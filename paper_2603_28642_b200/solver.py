@@ -12,12 +12,13 @@ are bit-identical to the reference's.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib as L
-from .device import device_matrix, device_preconditioner, device_solver
+from .device import DeviceSolver, device_matrix, device_preconditioner, device_solver, device_solvers
 
 
 @dataclass
@@ -130,7 +131,11 @@ def pcgls(A, b, pre, cfg: CglsConfig, iterate_hook=None):
                     break
     rep, hist = solver.finish(cfg.max_iters + cfg.estimator_delay + 2)
     solver.get_x(L.ptr(x), L.RSB_HOST)
-    report = SolveReport(
+    return x, _report(rep, hist, psize, nmod)
+
+
+def _report(rep, hist, psize, nmod) -> SolveReport:
+    return SolveReport(
         its=int(rep.its),
         converged=bool(rep.converged),
         breakdown=bool(rep.breakdown),
@@ -141,4 +146,51 @@ def pcgls(A, b, pre, cfg: CglsConfig, iterate_hook=None):
         residual_norm_final=float(rep.residual_norm),
         gradient_norm_final=float(rep.gradient_norm),
     )
-    return x, report
+
+
+def _check(A, pre, m):
+    n = int(A.ncols)
+    if pre is not None:
+        if pre.factors.nrows != int(A.nrows) or pre.n != n:
+            raise ValueError("preconditioner does not match the matrix")
+        return pre.psize, pre.factors.nmod
+    return 0, 0
+
+
+def pcgls_batch(A, B, pre, cfg: CglsConfig, streams: int | None = None):
+    """Independent pcgls solves of A x_j ~ B[j] sharing A and pre (config 4's
+    batch of right-hand sides per GPU).
+
+    Not in the reference API: the reference solves one b per pcgls call; the
+    result for each row of B is exactly pcgls(A, B[j], pre, cfg), bit for
+    bit.  The solves run concurrently, `streams` at a time (default: all),
+    each on its own CUDA stream with its own workspace, reading the one
+    device copy of A and the factors.  Returns (X with rows x_j, [reports]).
+    """
+    B = np.ascontiguousarray(np.atleast_2d(np.asarray(B, dtype=np.float64)))
+    m, n = int(A.nrows), int(A.ncols)
+    if B.ndim != 2 or B.shape[1] != m:
+        raise ValueError("right-hand side length mismatch")
+    psize, nmod = _check(A, pre, m)
+    k = B.shape[0]
+    X = np.empty((k, n))
+    reports: list[SolveReport] = []
+    if k == 0:
+        return X, reports
+    width = k if streams is None else max(1, min(int(streams), k))
+    dA = device_matrix(A)
+    dpre = device_preconditioner(pre, dA.ctx) if pre is not None else None
+    solvers = device_solvers(dA, dpre, width)
+    ccfg = DeviceSolver.cfg_struct(cfg.norm_A, cfg.delta, cfg.max_iters, cfg.estimator_delay, cfg.ratio_raw)
+    cap = cfg.max_iters + cfg.estimator_delay + 2
+    for lo in range(0, k, width):
+        c = min(width, k - lo)
+        hs = (ctypes.c_void_p * c)(*[s.h for s in solvers[:c]])
+        bs = (ctypes.c_void_p * c)(*[B[lo + i].ctypes.data for i in range(c)])
+        xs = (ctypes.c_void_p * c)(*[X[lo + i].ctypes.data for i in range(c)])
+        reps = (L.ReportC * c)()
+        hist = np.empty((c, cap))
+        L.check(L.lib().rsb_pcgls_many(c, hs, bs, L.RSB_HOST, ctypes.byref(ccfg), xs, reps, L.ptr(hist), cap))
+        for i in range(c):
+            reports.append(_report(reps[i], hist[i, : min(reps[i].history_len, cap)].copy(), psize, nmod))
+    return X, reports

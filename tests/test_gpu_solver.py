@@ -189,3 +189,41 @@ def test_row_partitioned_device_backend_single_rank_bitwise():
     assert np.array_equal(xd, x)
     assert repd.its == rep.its and repd.ratio_pt_history == rep.ratio_pt_history
     assert repd.residual_norm_final == rep.residual_norm_final
+
+
+@pytest.mark.parametrize("mode", ["cg", "dense", None])
+def test_pcgls_batch_equals_single_solves(mode):
+    """Concurrent solves on separate streams sharing A and the factors: each
+    equals the single-RHS pcgls bit for bit, including a zero RHS (stationary
+    start) and RHS that stop at different iterations."""
+    from paper_2603_28642_b200 import workloads as W
+
+    A, b = W.config0(seed=13, m=900, n=600)
+    S, _ = P.column_scale(A)
+    na = P.power_method_norm2(S, 100, 13)
+    pre = None
+    if mode is not None:
+        f = P.ilup_factorize(S, P.IlupParams(p=10, tau=1e-3, mu=1.0))
+        pre = P.build_preconditioner(f, s_mode=P.SMode(mode))
+    rng = np.random.default_rng(5)
+    B = np.stack([b, np.zeros_like(b), rng.standard_normal(b.size), S.to_dense() @ rng.standard_normal(S.ncols),
+                  rng.uniform(-1, 1, b.size)])
+    cfg = P.CglsConfig(norm_A=na, delta=1e-8, max_iters=150)
+    X, reps = P.pcgls_batch(S, B, pre, cfg)
+    X2, reps2 = P.pcgls_batch(S, B, pre, cfg, streams=2)
+    for j in range(B.shape[0]):
+        x, rep = P.pcgls(S, B[j], pre, cfg)
+        assert np.array_equal(X[j], x), j
+        assert reps[j].to_dict() == rep.to_dict(), j
+        assert np.array_equal(X2[j], x), j
+        assert reps2[j].to_dict() == rep.to_dict(), j
+    assert reps[1].its == 0 and reps[1].converged
+    assert len({r.its for r in reps}) > 1
+
+
+def test_pcgls_batch_validation():
+    A = P.CscMatrix.identity(4)
+    with pytest.raises(ValueError):
+        P.pcgls_batch(A, np.zeros((2, 3)), None, P.CglsConfig(norm_A=1.0))
+    X, reps = P.pcgls_batch(A, np.zeros((0, 4)), None, P.CglsConfig(norm_A=1.0))
+    assert X.shape == (0, 4) and reps == []
