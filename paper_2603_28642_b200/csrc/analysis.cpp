@@ -8,7 +8,9 @@
 // tasks by level and packs their entries in warp-interleaved slices (see
 // TriDev in rsb_internal.h) so the device solve reads them coalesced.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 
@@ -175,7 +177,9 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     // 16-byte shared loads) with the slice's longest task as its trip count
     std::vector<int64_t> sp;     // staged start of each level (multiple of 32)
     std::vector<int64_t> srb;    // record base of each staged slice (prefix sums of 32 * K)
-    int64_t ch = 0, emax = 0, ns = 0, maxw32 = 0;
+    std::vector<int32_t> posof;  // staged position of each unknown
+    int64_t ch = 0, emax = 0, ns = 0, maxw32 = 0, far = 0;
+    int32_t lean_n = 0;
     if (single_cta) {
         sp.assign(nlev + 1, 0);
         for (int32_t l = 0; l < nlev; ++l) {
@@ -184,6 +188,28 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             maxw32 = std::max(maxw32, (w + 31) / 32 * 32);
         }
         ns = sp[nlev];
+        posof.resize(n);
+        for (int32_t l = 0; l < nlev; ++l)
+            for (int64_t q = lstart[l]; q < lstart[l + 1]; ++q) posof[order[q]] = (int32_t)(sp[l] + (q - lstart[l]));
+        // dependencies older than the ring, longest task
+        int64_t maxlen = 0;
+        for (int32_t l = 0; l < nlev; ++l)
+            for (int64_t gq = lstart[l]; gq < lstart[l + 1]; ++gq) {
+                const int32_t t = order[gq];
+                const int64_t q = sp[l] + (gq - lstart[l]);
+                maxlen = std::max(maxlen, tptr[t + 1] - tptr[t]);
+                for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k)
+                    if (q - posof[ent[k].col] + maxw32 >= kRing) ++far;
+            }
+        // lean variant: one task per consumer thread and level, every task in
+        // registers (dot tasks of >= 16 entries take the blocked BLAS order,
+        // which the lean chain does not implement), no far dependencies
+        const char *lean_env = getenv("RSB_TRSV_LEAN");
+        if (!(lean_env && std::strcmp(lean_env, "0") == 0) && maxw32 <= kLeanMaxWidth && far == 0 &&
+            maxlen <= (is_dot ? 15 : kLeanMaxN))
+            lean_n = (int32_t)std::max<int64_t>(1, maxlen);
+        if (lean_n && getenv("RSB_LEAN_N_MIN"))  // experiments: longer chains than needed
+            lean_n = std::max<int32_t>(lean_n, std::min<int32_t>(is_dot ? 15 : 16, atoi(getenv("RSB_LEAN_N_MIN"))));
         const int64_t nsl = ns / 32;
         srb.assign(nsl + 1, 0);
         for (int32_t l = 0; l < nlev; ++l)
@@ -193,27 +219,30 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
                     const int64_t src_q = lstart[l] + (q - sp[l]);
                     if (src_q < lstart[l + 1]) K = std::max(K, tptr[order[src_q] + 1] - tptr[order[src_q]]);
                 }
-                srb[q0 / 32 + 1] = 32 * K;
+                // lean: entry slots padded to whole quads (sources are read 4 at a time)
+                srb[q0 / 32 + 1] = 32 * (lean_n ? (K + 3) & ~3LL : K);
             }
         for (int64_t w = 0; w < nsl; ++w) srb[w + 1] += srb[w];
+        const int64_t ch_max = getenv("RSB_STAGE_CH_MAX") ? atoll(getenv("RSB_STAGE_CH_MAX")) : 1024;  // experiments
         for (int64_t cand : {1024, 512, 256, 128}) {
+            if (cand > ch_max) continue;
             if (cand < maxw32) break;
             int64_t em = 0;
             for (int64_t c0 = 0; c0 < ns; c0 += cand) em = std::max(em, srb[std::min(ns, c0 + cand) / 32] - srb[c0 / 32]);
-            em = std::max<int64_t>(32, em);
-            if (stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand) <= kStageSmemBudget) {
+            em = std::max<int64_t>(128, em);
+            const int64_t bytes = lean_n ? lean_smem_bytes(cand, em, !unit, nlev)
+                                         : stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand);
+            if (bytes <= kStageSmemBudget) {
                 ch = cand;
                 emax = em;
                 break;
             }
         }
-        if (ch == 0) single_cta = false;
-    }
-    std::vector<int32_t> posof;  // staged position of each unknown
-    if (single_cta) {
-        posof.resize(n);
-        for (int32_t l = 0; l < nlev; ++l)
-            for (int64_t q = lstart[l]; q < lstart[l + 1]; ++q) posof[order[q]] = (int32_t)(sp[l] + (q - lstart[l]));
+        if (ch == 0) {
+            single_cta = false;
+            lean_n = 0;
+            far = 0;
+        }
     }
 
     std::vector<int32_t> ecol(slots, -1);
@@ -234,16 +263,27 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             if (!unit) tdiag[q] = diag[t];
         }
     }
-    // staged layout: per-position meta, {diag, 1/diag}, lane-interleaved records
-    // whose source is the ring byte offset of a live dependency or -(row + 2)
+    // staged layout: per-position meta, {diag, 1/diag}, entry records whose
+    // source is the ring byte offset of a live dependency or -(row + 2).
+    // Records are lane-interleaved per slice (entry q of lane l at
+    // slice_base + 32q + l), or, lean, values in lane pairs (entry q of lane l
+    // at slice_base + 64(q/2) + 2l + q%2) and sources in lane quads (at
+    // slice_base + 128(q/4) + 4l + q%4), zero past each task's length.
     std::vector<StageRec> recs;
+    std::vector<double> rval;
+    std::vector<int32_t> rsrc;
     std::vector<StageMeta> meta;
     std::vector<double> dd;
     std::vector<int64_t> croff;
     std::vector<int32_t> srows;
-    int64_t far = 0;
     if (single_cta) {
-        recs.assign(std::max<int64_t>(32, srb[ns / 32]), StageRec{0.0, 0, 0});
+        const int64_t nslots = std::max<int64_t>(128, srb[ns / 32]);
+        if (lean_n) {
+            rval.assign(nslots, 0.0);
+            rsrc.assign(nslots, 0);
+        } else {
+            recs.assign(nslots, StageRec{0.0, 0, 0});
+        }
         meta.assign(padded, StageMeta{-1, 0, 0, 0});
         srows.assign(padded, -1);
         croff.resize(nchunks + 1);
@@ -252,8 +292,13 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         for (int32_t l = 0; l < nlev; ++l) {
             for (int64_t q = sp[l]; q < sp[l + 1]; ++q) {
                 const int64_t sl = q / 32, lane = q & 31;
-                const int32_t K = (int32_t)((srb[sl + 1] - srb[sl]) / 32);
-                const int32_t roff = (int32_t)(srb[sl] - croff[q / ch] + lane);
+                int32_t K = 0;  // the slice's longest task
+                for (int64_t q2 = sl * 32; q2 < sl * 32 + 32; ++q2) {
+                    const int64_t g2 = lstart[l] + (q2 - sp[l]);
+                    if (g2 < lstart[l + 1]) K = std::max<int32_t>(K, (int32_t)(tptr[order[g2] + 1] - tptr[order[g2]]));
+                }
+                // lean: the slice base in its chunk; else the lane's first record
+                const int32_t roff = (int32_t)(srb[sl] - croff[q / ch] + (lean_n ? 0 : lane));
                 const int64_t gq = lstart[l] + (q - sp[l]);
                 if (gq >= lstart[l + 1]) {  // padding task
                     meta[q] = StageMeta{-1, 0, roff, K};
@@ -263,24 +308,31 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
                 for (int64_t k = tptr[t]; k < tptr[t + 1]; ++k) {
                     const int32_t col = ent[k].col;
                     const int64_t p = posof[col];
-                    int32_t src;
-                    if (q - p + maxw32 < kRing) {
-                        src = (int32_t)((p & (kRing - 1)) * 8);
+                    const int32_t src = (q - p + maxw32 < kRing) ? (int32_t)((p & (kRing - 1)) * 8) : -(col + 2);
+                    const int64_t e = k - tptr[t];
+                    if (lean_n) {
+                        rval[srb[sl] + (e >> 1) * 64 + lane * 2 + (e & 1)] = ent[k].val;
+                        rsrc[srb[sl] + (e >> 2) * 128 + lane * 4 + (e & 3)] = src;
                     } else {
-                        src = -(col + 2);
-                        ++far;
+                        recs[srb[sl] + e * 32 + lane] = StageRec{ent[k].val, src, 0};
                     }
-                    recs[srb[sl] + (k - tptr[t]) * 32 + lane] = StageRec{ent[k].val, src, 0};
                 }
                 meta[q] = StageMeta{t, (int32_t)(tptr[t + 1] - tptr[t]), roff, K};
                 srows[q] = t;
                 if (!unit) {
                     dd[2 * q] = diag[t];
-                    dd[2 * q + 1] = 1.0 / diag[t];  // correctly rounded reciprocal
+                    const double y = 1.0 / diag[t];  // correctly rounded reciprocal
+                    const double ad = std::fabs(diag[t]);
+                    // lean: y = 0 marks a diagonal outside the exact-division range
+                    dd[2 * q + 1] = (lean_n && !(ad > 0x1p-500 && ad < 0x1p500)) ? 0.0 : y;
                 }
             }
         }
     }
+    if (getenv("RSB_DEBUG_ANALYSIS"))
+        fprintf(stderr, "[rsb] tri kind=%d n=%lld levels=%d maxw=%lld single_cta=%d lean_n=%d far=%lld ch=%lld emax=%lld\n",
+                kind, (long long)n, nlev, (long long)maxw, (int)single_cta, lean_n, (long long)far, (long long)ch,
+                (long long)emax);
     std::vector<int32_t> rows(order.begin(), order.end());
     rows.resize(padded, 0);
     if (single_cta) rows = srows;  // the staged kernel's gather uses staged positions
@@ -300,9 +352,12 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     S->stage_emax = (int32_t)emax;
     S->nchunks = (int32_t)nchunks;
     S->padded_n = padded;
-    S->nrecs = (int64_t)recs.size();
+    S->nrecs = (int64_t)(lean_n ? rval.size() : recs.size());
+    S->lean_n = lean_n;
     int rc = RSB_OK;
-    if (S->single_cta && (rc = prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
+    if (S->single_cta &&
+        (rc = lean_n ? prepare_trsv_lean(lean_smem_bytes(ch, emax, !unit, nlev))
+                     : prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
         delete S;
         return rc;
     }
@@ -316,7 +371,9 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), tdiag.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->chunk_roff, croff.data(), croff.size())) != RSB_OK) ||
         (single_cta && (rc = dev_alloc(ctx, (void **)&S->bpos, padded * sizeof(double))) != RSB_OK) ||
-        (single_cta && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
+        (single_cta && !lean_n && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
+        (lean_n && (rc = dev_upload(ctx, &S->rval, rval.data(), rval.size())) != RSB_OK) ||
+        (lean_n && (rc = dev_upload(ctx, &S->rsrc, rsrc.data(), rsrc.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
@@ -348,6 +405,8 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->chunk_roff) dev_free(ctx, s->chunk_roff, (s->nchunks + 1) * sizeof(int64_t));
     if (s->bpos) dev_free(ctx, s->bpos, padded * sizeof(double));
     if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));
+    if (s->rval) dev_free(ctx, s->rval, s->nrecs * sizeof(double));
+    if (s->rsrc) dev_free(ctx, s->rsrc, s->nrecs * sizeof(int32_t));
     if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
     if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
     if (s->prof) dev_free(ctx, s->prof, 8 * sizeof(long long));

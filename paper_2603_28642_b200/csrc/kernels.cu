@@ -8,6 +8,7 @@
 
 #include <climits>
 
+#include "device_common.cuh"
 #include "rsb_internal.h"
 
 namespace rsb {
@@ -21,9 +22,6 @@ constexpr int kStageRegs = 16;
 constexpr int kDotChunk = 2048;  // elements per vector per stage of the staged exact dot
 constexpr int kDotStages = 3;  // entries per task held in registers by the staged solve
 
-__device__ __forceinline__ bool gated(const Gate &g) {
-    return (g.a && *(volatile const int *)g.a) || (g.b && *(volatile const int *)g.b);
-}
 
 __device__ __forceinline__ double vin(const VecIn &v, int64_t i) {
     return v.g ? v.p[v.g[i + v.off]] : v.p[i + v.off];
@@ -423,30 +421,6 @@ __device__ __forceinline__ double canonical(double v) {
 }
 
 // ---- shared-memory staging primitives (sm_90+: mbarrier + 1-D TMA bulk copy)
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
 
 // Exact-order dot for long contiguous vectors: the same single-warp OpenBLAS
 // association as k_dot_exact, with both operands streamed through shared
@@ -554,25 +528,6 @@ __device__ __noinline__ double rec_blas_dot(const StageRec *rec, int len, const 
     return dot;
 }
 
-// a / d correctly rounded, given y = RN(1/d): q0 = RN(a*y), r = a - q0*d
-// (exact, FMA), q1 = RN(q0 + r*y) (Markstein).  Valid while no intermediate
-// over/underflows -- guaranteed for |a|, |d| in (2^-500, 2^500); outside that
-// range (zeros, subnormals, non-finite values included) the IEEE division
-// runs instead.  24 cycles of dependent FP64 instead of ~400 for div.rn.f64
-// on sm_100 (scripts/probes/fp64_latency.cu); cross-checked bit for bit
-// against a/b on 2.8e9 random and adversarial operand pairs.
-__device__ __forceinline__ double exact_div(double a, double d, double y) {
-    const double aa = fabs(a), ad = fabs(d);
-    if (ad > 0x1p-500 && ad < 0x1p500) {
-        if (aa > 0x1p-500 && aa < 0x1p500) {
-            const double q0 = __dmul_rn(a, y);
-            const double r = fma(-q0, d, a);
-            return fma(r, y, q0);
-        }
-        if (a == 0.0) return __dmul_rn(a, y);  // +-0 with the quotient's sign, exactly as a / d
-    }
-    return __ddiv_rn(a, d);
-}
 
 // One staged task with at most N entries (N = the warp's longest task, so
 // the loop is unrolled for exactly that many): all record and ring loads are
@@ -663,10 +618,13 @@ __global__ void __launch_bounds__(kCtaTri + 32) k_trsv_stage(TriDev T, double *x
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x >= kCtaTri) {
+    // the producer is warp 3 (SMSP 3); the consumer slice it displaces, the
+    // rarely used 4th one, runs on warp 4 and shares SMSP 0 with the busiest
+    const int warp = threadIdx.x >> 5;
+    if (warp == 3) {
         // producer warp: chunk c goes to buffer c % kStageBufs once the
         // consumers released the chunk that held it; the consumers never issue
-        if (threadIdx.x == kCtaTri) {
+        if (threadIdx.x == 96) {
             for (int c = 0; c < nch; ++c) {
                 const int b = c & (kStageBufs - 1);
                 if (c >= kStageBufs) mbar_wait(&empty[b], (unsigned)(((c / kStageBufs) - 1) & 1));
@@ -685,6 +643,7 @@ __global__ void __launch_bounds__(kCtaTri + 32) k_trsv_stage(TriDev T, double *x
         return;
     }
     const int lane = threadIdx.x & 31;
+    const int slot = warp < 3 ? (int)threadIdx.x : (int)threadIdx.x - 32;
     int released = 0, ready = -1;
     long long pc[7] = {0, 0, 0, 0, 0, 0, 0}, tq = 0, tp = 0;
     const bool prof = T.prof && threadIdx.x == 0;
@@ -710,7 +669,7 @@ __global__ void __launch_bounds__(kCtaTri + 32) k_trsv_stage(TriDev T, double *x
             mbar_wait(&full[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
         }
         RSB_PROF(5)
-        for (int t = lo + threadIdx.x; t < hi; t += kCtaTri) {
+        for (int t = lo + slot; t < hi; t += kCtaTri) {
             const int loc = t & (CH - 1);
             const unsigned char *B = bufs + (size_t)((t >> lgch) & (kStageBufs - 1)) * bb;
             const StageMeta m = reinterpret_cast<const StageMeta *>(B + o_meta)[loc];
@@ -913,7 +872,9 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
                                                                           v.bpos, g);
         RSB_TRY(post_launch(ctx));
         const int sel = T.mode + (T.has_far ? 4 : 0);
-        switch (sel) {
+        if (T.lean_n) {
+            RSB_TRY(launch_trsv_lean(ctx, T, v, x, g));
+        } else switch (sel) {
             case 0: k_trsv_stage<0, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
             case 1: k_trsv_stage<1, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
             case 2: k_trsv_stage<2, false><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;

@@ -47,6 +47,9 @@ constexpr int64_t kCtaTriMaxMeanWidth = 4096;
 // slot written at position p is reused by position p + kRing, so a dependency
 // at distance d is still live if d + (widest level) < kRing.
 constexpr int kRing = 4096;
+// lean staged solve: widest level (one task per consumer thread) and longest task
+constexpr int64_t kLeanMaxWidth = 128;
+constexpr int64_t kLeanMaxN = 16;
 constexpr int kStageBufs = 4;
 constexpr int kStageSmemBudget = 220 * 1024;
 // shared-memory bytes of one staging buffer
@@ -64,6 +67,15 @@ struct alignas(16) StageRec {
     int32_t src;
     int32_t pad;
 };
+// lean variant: rhs, meta, [diag pair], values (8 B) and sources (4 B)
+inline int64_t lean_buf_bytes(int64_t ch, int64_t emax, bool diag) {
+    return ch * 8 + ch * 16 + (diag ? ch * 16 : 0) + emax * 12;
+}
+inline int64_t lean_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels) {
+    // ring, staging buffers, mbarriers, level bounds (nlevels + 4, padded to 4)
+    return (int64_t)kRing * 8 + kStageBufs * lean_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
+           ((nlevels + 8) & ~3LL) * 4;
+}
 inline int64_t stage_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels, int64_t nchunks) {
     // ring, staging buffers, mbarriers, level bounds (padded to 4), chunk record counts
     return (int64_t)kRing * 8 + kStageBufs * stage_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
@@ -137,6 +149,10 @@ struct TriDev {
     const int64_t *chunk_roff;  // first record of each chunk (nchunks + 1)
     double *bpos;               // right-hand side gathered into position order
     const StageRec *recs;       // entry records, contiguous per task in position order
+    // lean staged solve (lean_n > 0): entry values in lane pairs and sources in
+    // lane quads per 32-position slice (one 16-byte load per 2 / 4 entries)
+    const double *rval;
+    const int32_t *rsrc;
     const StageMeta *meta;      // per position (padded to nchunks * stage_ch)
     const double *ddiag;        // per position: {diag, RN(1/diag)} (staged solve's exact division)
     long long *prof;            // optional per-phase cycle counters (RSB_TRSV_PROFILE), else null
@@ -176,13 +192,18 @@ struct TriSched {
     int64_t padded_n = 0;  // task_row / diag / bpos / meta lengths (nchunks * stage_ch when staged)
     StageRec *recs = nullptr;
     int64_t nrecs = 0;
+    // lean variant: every task holds at most lean_n entries, levels are at most
+    // kCtaTri wide and no dependency is older than the ring; 0 = not lean
+    int32_t lean_n = 0;
+    double *rval = nullptr;
+    int32_t *rsrc = nullptr;
     StageMeta *meta = nullptr;
     double *ddiag = nullptr;
     long long *prof = nullptr;  // 8 counters, allocated when RSB_TRSV_PROFILE is set
     TriDev view() const {
         return TriDev{n,       mode,       task_row, slice_off,  ecol, eval, diag,   ticket,
                       has_far, (int32_t)nlevels,     level_ptr, stage_ch, stage_emax, nchunks,
-                      chunk_roff, bpos,    recs,     meta,       ddiag, prof};
+                      chunk_roff, bpos,    recs,     rval,       rsrc,  meta, ddiag, prof};
     }
 };
 
@@ -259,6 +280,8 @@ int finish_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s);
 int get_tri(rsb_mat *T, int kind, TriSched **out);
 // one-time kernel attribute setup for the single-CTA triangular solve of order n
 int prepare_trsv_cta(int64_t n);
+int prepare_trsv_lean(int64_t smem_bytes);
+int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
 // one-time kernel attribute setup for the dense S solve of size s
 int prepare_chol(int64_t s);
 // one-time kernel attribute setup at context creation (dynamic shared memory)

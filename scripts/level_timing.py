@@ -22,5 +22,5 @@ for name, M, kind in (("L1", f.L1, L.TRI_LOWER_UNIT), ("L1T", f.L1, L.TRI_LOWER_
     c = (ctypes.c_longlong * 8)()
     L.check(L.lib().rsb_trsv_profile(dm.h, kind, c))
     nl = c[5]
-    out[name] = {k: round(c[i] / nl, 1) for i, k in [(0, "control+issue"), (6, "mbar_wait"), (1, "header"), (2, "chain"), (3, "div+store"), (4, "barrier+loop")]}
+    out[name] = {k: round(c[i] / nl, 1) for i, k in [(0, "top+await"), (1, "loads+prefetch+chain"), (2, "div+store"), (3, "extra+release"), (4, "barrier+rotate")]}
 print(json.dumps(out))
