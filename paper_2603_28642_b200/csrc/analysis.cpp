@@ -211,31 +211,42 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         if (lean_n && getenv("RSB_LEAN_N_MIN"))  // experiments: longer chains than needed
             lean_n = std::max<int32_t>(lean_n, std::min<int32_t>(is_dot ? 15 : 16, atoi(getenv("RSB_LEAN_N_MIN"))));
         const int64_t nsl = ns / 32;
-        srb.assign(nsl + 1, 0);
-        for (int32_t l = 0; l < nlev; ++l)
-            for (int64_t q0 = sp[l]; q0 < sp[l + 1]; q0 += 32) {
-                int64_t K = 0;
-                for (int64_t q = q0; q < q0 + 32; ++q) {
-                    const int64_t src_q = lstart[l] + (q - sp[l]);
-                    if (src_q < lstart[l + 1]) K = std::max(K, tptr[order[src_q] + 1] - tptr[order[src_q]]);
-                }
-                // lean: entry slots padded to whole quads (sources are read 4 at a time)
-                srb[q0 / 32 + 1] = 32 * (lean_n ? (K + 3) & ~3LL : K);
-            }
-        for (int64_t w = 0; w < nsl; ++w) srb[w + 1] += srb[w];
         const int64_t ch_max = getenv("RSB_STAGE_CH_MAX") ? atoll(getenv("RSB_STAGE_CH_MAX")) : 1024;  // experiments
-        for (int64_t cand : {1024, 512, 256, 128}) {
-            if (cand > ch_max) continue;
-            if (cand < maxw32) break;
-            int64_t em = 0;
-            for (int64_t c0 = 0; c0 < ns; c0 += cand) em = std::max(em, srb[std::min(ns, c0 + cand) / 32] - srb[c0 / 32]);
-            em = std::max<int64_t>(128, em);
-            const int64_t bytes = lean_n ? lean_smem_bytes(cand, em, !unit, nlev)
-                                         : stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand);
-            if (bytes <= kStageSmemBudget) {
-                ch = cand;
-                emax = em;
-                break;
+        // record layout and chunk size; a lean schedule whose chunks do not
+        // fit falls back to the general staged layout
+        for (int attempt = 0; attempt < 2 && ch == 0; ++attempt) {
+            if (attempt == 1) {
+                if (!lean_n) break;
+                lean_n = 0;
+            }
+            srb.assign(nsl + 1, 0);
+            for (int32_t l = 0; l < nlev; ++l)
+                for (int64_t q0 = sp[l]; q0 < sp[l + 1]; q0 += 32) {
+                    int64_t K = 0;
+                    for (int64_t q = q0; q < q0 + 32; ++q) {
+                        const int64_t src_q = lstart[l] + (q - sp[l]);
+                        if (src_q < lstart[l + 1]) K = std::max(K, tptr[order[src_q] + 1] - tptr[order[src_q]]);
+                    }
+                    // lean: entry slots padded to whole quads (sources are read 4 at a time)
+                    srb[q0 / 32 + 1] = 32 * (lean_n ? (K + 3) & ~3LL : K);
+                }
+            for (int64_t w = 0; w < nsl; ++w) srb[w + 1] += srb[w];
+            for (int64_t cand : {1024, 512, 256, 128}) {
+                if (cand > ch_max) continue;
+                if (cand < maxw32) break;
+                int64_t em = 0;
+                for (int64_t c0 = 0; c0 < ns; c0 += cand)
+                    em = std::max(em, srb[std::min(ns, c0 + cand) / 32] - srb[c0 / 32]);
+                em = std::max<int64_t>(128, em);
+                const int64_t lslots = (lean_n + 3) & ~3;  // lean: uniform entry slots per task
+                if (lean_n) em = cand * lslots;
+                const int64_t bytes = lean_n ? lean_dyn_smem_bytes(cand, lslots, !unit, nlev) + kLeanRingBytes
+                                             : stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand);
+                if (bytes <= kStageSmemBudget) {
+                    ch = cand;
+                    emax = em;
+                    break;
+                }
             }
         }
         if (ch == 0) {
@@ -276,11 +287,16 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     std::vector<double> dd;
     std::vector<int64_t> croff;
     std::vector<int32_t> srows;
+    const int64_t lslots = (lean_n + 3) & ~3;
     if (single_cta) {
         const int64_t nslots = std::max<int64_t>(128, srb[ns / 32]);
         if (lean_n) {
-            rval.assign(nslots, 0.0);
-            rsrc.assign(nslots, 0);
+            // uniform slots: entry e of the task at position q at
+            // (q - lane) * lslots + 64 (e / 2) + 2 lane + e % 2 (values) and
+            // (q - lane) * lslots + 128 (e / 4) + 4 lane + e % 4 (sources);
+            // empty slots read the ring's zero slot
+            rval.assign(padded * lslots, 0.0);
+            rsrc.assign(padded * lslots, (int32_t)(kRing * 8));
         } else {
             recs.assign(nslots, StageRec{0.0, 0, 0});
         }
@@ -311,8 +327,9 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
                     const int32_t src = (q - p + maxw32 < kRing) ? (int32_t)((p & (kRing - 1)) * 8) : -(col + 2);
                     const int64_t e = k - tptr[t];
                     if (lean_n) {
-                        rval[srb[sl] + (e >> 1) * 64 + lane * 2 + (e & 1)] = ent[k].val;
-                        rsrc[srb[sl] + (e >> 2) * 128 + lane * 4 + (e & 3)] = src;
+                        const int64_t base = (q - lane) * lslots;
+                        rval[base + (e >> 1) * 64 + lane * 2 + (e & 1)] = ent[k].val;
+                        rsrc[base + (e >> 2) * 128 + lane * 4 + (e & 3)] = src;
                     } else {
                         recs[srb[sl] + e * 32 + lane] = StageRec{ent[k].val, src, 0};
                     }
@@ -329,10 +346,38 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             }
         }
     }
+    // lean segment plan: the consumers' chunk bookkeeping between runs of
+    // levels (see k_trsv_lean); iteration l prefetches level l + 1, i.e.
+    // reads positions below lvl[l + 2], the level bounds padded with the end
+    std::vector<int4> segs;
+    if (lean_n) {
+        auto L = [&](int64_t i) { return (int64_t)(i <= nlev ? sp[i] : sp[nlev]); };
+        const int64_t nch = nchunks;
+        int64_t released = 0, ready = (std::max<int64_t>(L(1) - 1, 0)) / ch;  // prologue: level 0
+        // chunks awaited beyond the released ones at a segment start (longer
+        // segments against waiting on a chunk still in flight)
+        const int64_t ahead = getenv("RSB_LEAN_AHEAD") ? atoll(getenv("RSB_LEAN_AHEAD")) : kStageBufs - 2;
+        int64_t l = 0;
+        while (l < nlev) {
+            released = std::max(released, L(l) / ch);  // released level by level in the kernel
+            const int64_t need = (L(l + 3) - 1) / ch;  // iterations l, l+1 prefetch levels l+1, l+2
+            // also the chunks issued a segment ago (landed by now), for longer segments
+            int64_t a = std::max(need, std::min(released + ahead, nch - 1));
+            a = std::min(a, released + kStageBufs - 1);
+            ready = std::max(ready, a);
+            const int64_t ready_end = (ready + 1) * ch;
+            int64_t lend = l;
+            while (lend + 2 <= nlev && L(lend + 3) <= ready_end) lend += 2;
+            if (lend == l) lend = l + 1;  // the last level (nlev odd)
+            segs.push_back(make_int4((int)l, (int)lend, (int)released, (int)ready));
+            l = lend;
+        }
+    }
     if (getenv("RSB_DEBUG_ANALYSIS"))
-        fprintf(stderr, "[rsb] tri kind=%d n=%lld levels=%d maxw=%lld single_cta=%d lean_n=%d far=%lld ch=%lld emax=%lld\n",
+        fprintf(stderr, "[rsb] tri kind=%d n=%lld levels=%d maxw=%lld single_cta=%d lean_n=%d far=%lld ch=%lld emax=%lld "
+                "segments=%zu\n",
                 kind, (long long)n, nlev, (long long)maxw, (int)single_cta, lean_n, (long long)far, (long long)ch,
-                (long long)emax);
+                (long long)emax, segs.size());
     std::vector<int32_t> rows(order.begin(), order.end());
     rows.resize(padded, 0);
     if (single_cta) rows = srows;  // the staged kernel's gather uses staged positions
@@ -353,10 +398,12 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     S->nchunks = (int32_t)nchunks;
     S->padded_n = padded;
     S->nrecs = (int64_t)(lean_n ? rval.size() : recs.size());
+    if (lean_n) S->stage_emax = (int32_t)(ch * lslots);
     S->lean_n = lean_n;
+    S->lean_nseg = (int32_t)segs.size();
     int rc = RSB_OK;
     if (S->single_cta &&
-        (rc = lean_n ? prepare_trsv_lean(lean_smem_bytes(ch, emax, !unit, nlev))
+        (rc = lean_n ? prepare_trsv_lean(lean_dyn_smem_bytes(ch, lslots, !unit, nlev))
                      : prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
         delete S;
         return rc;
@@ -374,6 +421,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (single_cta && !lean_n && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rval, rval.data(), rval.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rsrc, rsrc.data(), rsrc.size())) != RSB_OK) ||
+        (lean_n && (rc = dev_upload(ctx, &S->lean_seg, segs.data(), segs.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
@@ -407,6 +455,7 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));
     if (s->rval) dev_free(ctx, s->rval, s->nrecs * sizeof(double));
     if (s->rsrc) dev_free(ctx, s->rsrc, s->nrecs * sizeof(int32_t));
+    if (s->lean_seg) dev_free(ctx, s->lean_seg, s->lean_nseg * sizeof(int4));
     if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
     if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
     if (s->prof) dev_free(ctx, s->prof, 8 * sizeof(long long));

@@ -36,6 +36,15 @@ static __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsign
         "r"(parity)
         : "memory");
 }
+// busy-polling wait (mbarrier.test_wait never suspends the thread; try_wait
+// may sleep past the phase flip, which puts wake-up latency on a critical path)
+static __device__ __forceinline__ void mbar_wait_spin(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 
 // a / d correctly rounded, given y = RN(1/d): q0 = RN(a*y), r = a - q0*d
 // (exact, FMA), q1 = RN(q0 + r*y) (Markstein).  Valid while no intermediate

@@ -67,15 +67,21 @@ struct alignas(16) StageRec {
     int32_t src;
     int32_t pad;
 };
-// lean variant: rhs, meta, [diag pair], values (8 B) and sources (4 B)
-inline int64_t lean_buf_bytes(int64_t ch, int64_t emax, bool diag) {
-    return ch * 8 + ch * 16 + (diag ? ch * 16 : 0) + emax * 12;
+// lean variant: every task owns ns = round4(N) entry slots (zero-padded);
+// per position: rhs (8 B), row (4 B), [diag pair] (16 B), entry values
+// (8 B each) and sources (4 B each)
+inline int64_t lean_buf_bytes(int64_t ch, int64_t ns, bool diag) {
+    return ch * (8 + 4 + (diag ? 16 : 0) + ns * 12);
 }
-inline int64_t lean_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels) {
-    // ring, staging buffers, mbarriers, level bounds (nlevels + 4, padded to 4)
-    return (int64_t)kRing * 8 + kStageBufs * lean_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
-           ((nlevels + 8) & ~3LL) * 4;
+// upper bound of the lean solve's segment count (segments cover >= 2 levels but the last)
+inline int64_t lean_max_segments(int64_t nlevels) { return nlevels / 2 + 2; }
+// dynamic shared memory: staging buffers, mbarriers, level bounds (nlevels + 5,
+// padded to 4), segment plan; the value ring is a static array
+inline int64_t lean_dyn_smem_bytes(int64_t ch, int64_t ns, bool diag, int64_t nlevels) {
+    return kStageBufs * lean_buf_bytes(ch, ns, diag) + 2 * kStageBufs * 8 + ((nlevels + 8) & ~3LL) * 4 +
+           lean_max_segments(nlevels) * 16;
 }
+constexpr int64_t kLeanRingBytes = (int64_t)(kRing + 2) * 8;  // ring + a zero slot (+ pad)
 inline int64_t stage_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels, int64_t nchunks) {
     // ring, staging buffers, mbarriers, level bounds (padded to 4), chunk record counts
     return (int64_t)kRing * 8 + kStageBufs * stage_buf_bytes(ch, emax, diag) + 2 * kStageBufs * 8 +
@@ -153,6 +159,10 @@ struct TriDev {
     // lane quads per 32-position slice (one 16-byte load per 2 / 4 entries)
     const double *rval;
     const int32_t *rsrc;
+    // segment plan {first level, end level, released chunks (info), await chunk}
+    const int4 *lean_seg;
+    int32_t lean_nseg;
+    int32_t stage_lgch;  // log2(stage_ch)
     const StageMeta *meta;      // per position (padded to nchunks * stage_ch)
     const double *ddiag;        // per position: {diag, RN(1/diag)} (staged solve's exact division)
     long long *prof;            // optional per-phase cycle counters (RSB_TRSV_PROFILE), else null
@@ -197,13 +207,20 @@ struct TriSched {
     int32_t lean_n = 0;
     double *rval = nullptr;
     int32_t *rsrc = nullptr;
+    int4 *lean_seg = nullptr;
+    int32_t lean_nseg = 0;
     StageMeta *meta = nullptr;
     double *ddiag = nullptr;
     long long *prof = nullptr;  // 8 counters, allocated when RSB_TRSV_PROFILE is set
+    int32_t lgch() const {
+        int32_t k = 0;
+        while (stage_ch > 0 && (1 << k) < stage_ch) ++k;
+        return k;
+    }
     TriDev view() const {
         return TriDev{n,       mode,       task_row, slice_off,  ecol, eval, diag,   ticket,
                       has_far, (int32_t)nlevels,     level_ptr, stage_ch, stage_emax, nchunks,
-                      chunk_roff, bpos,    recs,     rval,       rsrc,  meta, ddiag, prof};
+                      chunk_roff, bpos,    recs,     rval,       rsrc,  lean_seg, lean_nseg, lgch(), meta, ddiag, prof};
     }
 };
 

@@ -28,8 +28,9 @@
 //     the rare operand outside its range (zero excepted) takes IEEE division
 //     behind one warp vote;
 //   - task data arrives by 1-D TMA bulk copies into kStageBufs chunk buffers
-//     (producer warp); the consumers release and await chunks only between
-//     segments of levels that the resident chunks cover, never per level;
+//     (producer warp); a consumer warp releases a chunk with a predicated
+//     arrive in the level where it is used up, and awaits chunks only
+//     between segments of levels that the resident chunks cover (host plan);
 //   - two task buffers alternate (level loop unrolled by two), so nothing is
 //     copied between registers.
 #include <cuda_runtime.h>
@@ -46,28 +47,7 @@ constexpr int kLeanThreads = kLeanConsumers + 32;
 constexpr int kLeanProducerWarp = 3;  // SMSP 3; the rarely used 4th slice runs on warp 4
 static_assert(kLeanMaxWidth == kLeanConsumers, "one task per consumer thread and level");
 
-// predicated shared-memory accesses: the destination keeps its value when p
-// is false (no branch)
-__device__ __forceinline__ void lds_f64_if(bool p, unsigned a, double &v) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}"
-                 : "+d"(v)
-                 : "r"(a), "r"((int)p));
-}
-__device__ __forceinline__ void lds_v2f64_if(bool p, unsigned a, double2 &v) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%2];\n}"
-                 : "+d"(v.x), "+d"(v.y)
-                 : "r"(a), "r"((int)p));
-}
-__device__ __forceinline__ void lds_v4_if(bool p, unsigned a, int4 &v) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n @q ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];\n}"
-                 : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-                 : "r"(a), "r"((int)p));
-}
-__device__ __forceinline__ void sts_f64_if(bool p, unsigned a, double v) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}" ::"r"(a), "d"(v),
-                 "r"((int)p)
-                 : "memory");
-}
+// predicated global store (no branch)
 __device__ __forceinline__ void stg_f64_if(bool p, double *a, double v) {
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f64 [%0], %1;\n}" ::"l"(a), "d"(v),
                  "r"((int)p)
@@ -79,33 +59,69 @@ __device__ __forceinline__ void stg_f64_if(bool p, double *a, double v) {
 // level's critical path
 __device__ __noinline__ double ieee_div(double a, double d) { return __ddiv_rn(a, d); }
 
-template <int N>
+template <int NS>
 struct LeanTask {
-    int4 m;  // {row (-1 padding, -2 no task), len, slice base in its chunk, slice's longest task}
-    int src[4 * ((N + 3) / 4)];
-    double v[2 * ((N + 1) / 2)];
+    int row;     // unknown written (-1 padding position, -2 no task)
     double acc;  // right-hand side (gathered)
     double2 dr;  // {diag, RN(1/diag)}; 1/diag = 0 marks a diagonal outside the exact range
+    int src[NS];  // ring byte offsets (the zero slot past the task's length)
+    double v[NS];
 };
+
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_v4(unsigned a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_v2f64(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+// acc - p unless x == 0 (the entry is skipped: sc.py:261-262 adds nothing
+// for a zero unknown), as one predicated subtraction; NaN is not zero
+// (unordered compare, as C's x != 0)
+__device__ __forceinline__ double sub_unless_zero(double acc, double p, double x) {
+    asm("{\n .reg .pred q;\n setp.neu.f64 q, %2, 0d0000000000000000;\n @q sub.rn.f64 %0, %0, %1;\n}"
+        : "+d"(acc)
+        : "d"(p), "d"(x));
+    return acc;
+}
 
 template <int MODE, int N>
 __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x, Gate g) {
     if (gated(g)) return;
-    extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool kDiag = (MODE & 2) != 0;
-    constexpr int NQ = (N + 3) / 4, NP = (N + 1) / 2;
-    const int CH = T.stage_ch, EM = T.stage_emax;
-    unsigned char *bufs = smem + (size_t)kRing * 8;
-    const unsigned o_meta = (unsigned)CH * 8, o_dd = o_meta + (unsigned)CH * 16,
-                   o_val = o_dd + (kDiag ? (unsigned)CH * 16 : 0u), o_src = o_val + (unsigned)EM * 8,
-                   bb = o_src + (unsigned)EM * 4;
+    constexpr int NS = 4 * ((N + 3) / 4), NQ = NS / 4, NP = NS / 2;
+    __shared__ __align__(16) double ring[kRing + 2];  // values by task position; ring[kRing] = 0
+    __shared__ __align__(16) int zsrc[NS * 32];       // sources of a lane without a task: the zero slot
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int CH = T.stage_ch, lgch = T.stage_lgch;
+    unsigned char *bufs = smem;
+    const unsigned o_row = (unsigned)CH * 8, o_dd = o_row + (unsigned)CH * 4,
+                   o_val = o_dd + (kDiag ? (unsigned)CH * 16 : 0u), o_src = o_val + (unsigned)CH * NS * 8,
+                   bb = o_src + (unsigned)CH * NS * 4;
     unsigned long long *full = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * (size_t)bb);
     unsigned long long *empty = full + kStageBufs;
     int *lvl = reinterpret_cast<int *>(empty + kStageBufs);
-    const int nlev = T.nlevels, nch = T.nchunks, lgch = __ffs(CH) - 1;
-    // level bounds, padded with the end so lvl[l + 3] is always valid
+    const int nlev = T.nlevels, nch = T.nchunks;
+    int4 *seg = reinterpret_cast<int4 *>(lvl + ((nlev + 8) & ~3));
+    // level bounds, padded with the end so lvl[l + 2] is always valid
     for (int i = threadIdx.x; i <= nlev + 4; i += blockDim.x) lvl[i] = T.level_ptr[i < nlev ? i : nlev];
+    for (int i = threadIdx.x; i < T.lean_nseg; i += blockDim.x) seg[i] = T.lean_seg[i];
+    for (int i = threadIdx.x; i < NS * 32; i += blockDim.x) zsrc[i] = kRing * 8;
     if (threadIdx.x == 0) {
+        ring[kRing] = 0.0;
         for (int b = 0; b < kStageBufs; ++b) {
             mbar_init(&full[b], 1);
             mbar_init(&empty[b], kLeanConsumers / 32);
@@ -118,22 +134,19 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         // chunk c goes to buffer c % kStageBufs once the consumers released
         // the chunk that held it
         if (lane == 0) {
+            const unsigned bytes = bb;
             for (int c = 0; c < nch; ++c) {
                 const int b = c & (kStageBufs - 1);
-                if (c >= kStageBufs) mbar_wait(&empty[b], (unsigned)(((c / kStageBufs) - 1) & 1));
+                if (c >= kStageBufs) mbar_wait_spin(&empty[b], (unsigned)(((c / kStageBufs) - 1) & 1));
                 unsigned char *B = bufs + (size_t)b * bb;
-                const int64_t r0 = T.chunk_roff[c];
-                const int ne = (int)(T.chunk_roff[c + 1] - r0);
-                const unsigned bytes = (unsigned)(CH * 8 + CH * 16 + (kDiag ? CH * 16 : 0) + ne * 12);
+                const int64_t p0 = (int64_t)c * CH;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&full[b], bytes);
-                bulk_g2s(B, T.bpos + (int64_t)c * CH, CH * 8, &full[b]);
-                bulk_g2s(B + o_meta, T.meta + (int64_t)c * CH, CH * 16, &full[b]);
-                if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * (int64_t)c * CH, CH * 16, &full[b]);
-                if (ne) {
-                    bulk_g2s(B + o_val, T.rval + r0, (unsigned)ne * 8, &full[b]);
-                    bulk_g2s(B + o_src, T.rsrc + r0, (unsigned)ne * 4, &full[b]);
-                }
+                bulk_g2s(B, T.bpos + p0, CH * 8, &full[b]);
+                bulk_g2s(B + o_row, T.task_row + p0, CH * 4, &full[b]);
+                if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * p0, CH * 16, &full[b]);
+                bulk_g2s(B + o_val, T.rval + p0 * NS, (unsigned)CH * NS * 8, &full[b]);
+                bulk_g2s(B + o_src, T.rsrc + p0 * NS, (unsigned)CH * NS * 4, &full[b]);
             }
         }
         return;
@@ -141,41 +154,33 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     const int slot = warp < kLeanProducerWarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
     // shared-window bases, opaque so they stay in registers (not
     // rematerialised from SR_CgaCtaId every level)
-    unsigned s_ring, s_bufs;
-    asm volatile("mov.u32 %0, %1;" : "=r"(s_ring) : "r"(smem_u32(smem)));
+    unsigned s_ring, s_bufs, s_empty;
+    asm volatile("mov.u32 %0, %1;" : "=r"(s_ring) : "r"(smem_u32(ring)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_bufs) : "r"(smem_u32(bufs)));
-    int released = 0, ready = -1;
+    asm volatile("mov.u32 %0, %1;" : "=r"(s_empty) : "r"(smem_u32(empty)));
+    unsigned s_zsrc;
+    asm volatile("mov.u32 %0, %1;" : "=r"(s_zsrc) : "r"(smem_u32(zsrc)));
+    int ready = -1;
     auto await_chunk = [&](int c) {
-        for (; ready < c; ) {
+        for (; ready < c;) {
             ++ready;
-            mbar_wait(&full[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
+            mbar_wait_spin(&full[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
         }
     };
-    auto release_below = [&](int c) {
-        for (; released < c; ++released)
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                 smem_u32(&empty[released & (kStageBufs - 1)]))
-                             : "memory");
-    };
-    auto sbuf = [&](int t) -> unsigned { return s_bufs + (unsigned)((t >> lgch) & (kStageBufs - 1)) * bb; };
-    auto load_meta = [&](int t, int hi) -> int4 {
-        int4 m = make_int4(-2, 0, 0, 0);
-        lds_v4_if(t < hi, sbuf(t) + o_meta + (unsigned)(t & (CH - 1)) * 16, m);
-        return m;
-    };
-    // the rest of task t (its meta already in S.m): sources in quads, values
-    // in pairs, rhs, diagonal; nothing past the task's length is loaded
-    auto load_task = [&](LeanTask<N> &S, int t) {
-        const int len = S.m.y;
-        const bool has = S.m.x != -2;
-        const unsigned B = sbuf(t), loc = (unsigned)(t & (CH - 1));
-        const unsigned sa = B + o_src + (unsigned)(S.m.z + lane * 4) * 4;
-        const unsigned va = B + o_val + (unsigned)(S.m.z + lane * 2) * 8;
+    // all of the task at position t, unconditionally; a lane without a task
+    // (a position past the level, possibly in a chunk not yet landed) reads
+    // its sources from zsrc, the rest is loaded and never published
+    auto load_task = [&](LeanTask<NS> &S, int t, bool has) {
+        const unsigned B = s_bufs + (unsigned)((t >> lgch) & (kStageBufs - 1)) * bb;
+        const unsigned loc = (unsigned)(t & (CH - 1)), base = (loc - (unsigned)lane) * NS;
+        const int row = lds_s32(B + o_row + loc * 4);
+        S.row = has ? row : -2;
+        S.acc = lds_f64(B + loc * 8);
+        S.dr = kDiag ? lds_v2f64(B + o_dd + loc * 16) : make_double2(1.0, 1.0);
+        const unsigned sa = has ? B + o_src + base * 4 : s_zsrc;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            int4 s4 = make_int4(0, 0, 0, 0);
-            lds_v4_if(4 * q < len, sa + q * 512, s4);
+            const int4 s4 = lds_v4(sa + (q * 128 + lane * 4) * 4);
             S.src[4 * q] = s4.x;
             S.src[4 * q + 1] = s4.y;
             S.src[4 * q + 2] = s4.z;
@@ -183,45 +188,34 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         }
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            double2 v2 = make_double2(0.0, 0.0);
-            lds_v2f64_if(2 * q < len, va + q * 512, v2);
+            const double2 v2 = lds_v2f64(B + o_val + (base + q * 64 + lane * 2) * 8);
             S.v[2 * q] = v2.x;
             S.v[2 * q + 1] = v2.y;
         }
-        S.acc = 0.0;
-        lds_f64_if(has, B + loc * 8, S.acc);
-        S.dr = make_double2(1.0, 1.0);
-        if (kDiag) lds_v2f64_if(has, B + o_dd + loc * 16, S.dr);
     };
 
-    int lo = lvl[0], hi = lvl[1], hi1 = lvl[2];
-    auto level = [&](int l, LeanTask<N> &C, LeanTask<N> &Nx) {
-        const int hi2 = lvl[l + 3];  // end of level l + 2
+    int lo = lvl[0], hi = lvl[1];
+    auto level = [&](int l, LeanTask<NS> &C, LeanTask<NS> &Nx) {
+        const int hi1 = lvl[l + 2];  // end of level l + 1
         const int t = lo + slot;
-        // 1. this level's dependency loads
+        // 1. this level's dependency loads (the only loads on the chain)
         double xv[N];
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-            xv[q] = 0.0;
-            lds_f64_if(q < C.m.y, s_ring + (unsigned)C.src[q], xv[q]);
-        }
-        // 2. the next levels' task data (independent of this level's values)
-        load_task(Nx, hi + slot);
-        const int4 mm = load_meta(hi1 + slot, hi2);
+        for (int q = 0; q < N; ++q) xv[q] = lds_f64(s_ring + (unsigned)C.src[q]);
+        // 2. the next level's task (independent of this level's values)
+        load_task(Nx, hi + slot, hi + slot < hi1);
         // 3. the ordered chain (sc.py:261-262 sequential axpy order, or the
-        //    OpenBLAS ddot order for < 16 entries, sc.py:291)
+        //    OpenBLAS ddot order for < 16 entries, sc.py:291); empty slots
+        //    read the zero slot and change nothing
         double acc = C.acc;
         if (!(MODE & 1)) {
-            double pr[N];
 #pragma unroll
-            for (int q = 0; q < N; ++q) pr[q] = xv[q] != 0.0 ? __dmul_rn(C.v[q], xv[q]) : 0.0;
-#pragma unroll
-            for (int q = 0; q < N; ++q) acc = __dsub_rn(acc, pr[q]);
+            for (int q = 0; q < N; ++q) acc = sub_unless_zero(acc, __dmul_rn(C.v[q], xv[q]), xv[q]);
         } else {
             double dot = 0.0;
 #pragma unroll
             for (int q = 0; q < N; ++q) dot = fma(C.v[q], xv[q], dot);
-            acc = __dsub_rn(acc, dot);  // len 0: acc - (+0) = acc, also for -0
+            acc = __dsub_rn(acc, dot);  // an empty task: acc - (+0) = acc, also for -0
         }
         // 4. exact division (see exact_div), branch-free
         if (kDiag) {
@@ -231,46 +225,64 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
             const double q1 = fma(r, y, q0);
             const unsigned e = ((unsigned)__double2hiint(acc) >> 20) & 0x7ffu;
             const bool aok = e - 524u <= 998u;  // 2^-499 <= |acc| < 2^500
-            const bool bad = C.m.x >= 0 && (y == 0.0 || (!aok && acc != 0.0));
+            const bool bad = C.row >= 0 && (y == 0.0 || (!aok && acc != 0.0));
             double res = aok ? q1 : q0;  // acc == 0: q0 = +-0 with the quotient's sign
             if (__any_sync(0xffffffffu, bad)) {
                 if (bad) res = ieee_div(acc, d);
             }
-            if (C.m.x >= 0) acc = res;
+            if (C.row >= 0) acc = res;
         }
         // 5. publish
-        sts_f64_if(C.m.x != -2, s_ring + (unsigned)(t & (kRing - 1)) * 8, acc);
-        stg_f64_if(C.m.x >= 0, x + (C.m.x >= 0 ? C.m.x : 0), acc);
+        if (C.row != -2) ring[(t & (kRing - 1))] = acc;
+        stg_f64_if(C.row >= 0, x + (C.row >= 0 ? C.row : 0), acc);
+        // 6. a chunk that ends inside this level is done with (its loads were
+        //    consumed by this level's chain)
+        {
+            const int c0 = lo >> lgch;
+            const bool cross = lane == 0 && (hi >> lgch) != c0;
+            asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(
+                             s_empty + (unsigned)(c0 & (kStageBufs - 1)) * 8),
+                         "r"((int)cross)
+                         : "memory");
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kLeanConsumers) : "memory");
-        C.m = mm;  // C now waits for level l + 2
         lo = hi;
         hi = hi1;
-        hi1 = hi2;
     };
 
-    LeanTask<N> A, Bt;
-    await_chunk((lvl[2] - 1 >= 0 ? lvl[2] - 1 : 0) >> lgch);
-    A.m = load_meta(lo + slot, hi);
-    load_task(A, lo + slot);
-    Bt.m = load_meta(hi + slot, hi1);
-    int l = 0;
-    while (l < nlev) {
-        // segment: level l is in registers; iteration l' reads positions
-        // below lvl[l' + 3].  Chunks wholly before level l + 1 are done with.
-        release_below(hi >> lgch);
-        await_chunk((lvl[l + 4] - 1) >> lgch);  // the next pair
-        const int ready_end = (ready + 1) << lgch;
-        int lend = l;
-        while (lend + 2 <= nlev && lvl[lend + 4] <= ready_end) lend += 2;
-        if (lend == l) {  // the last level (nlev odd)
-            level(l, A, Bt);
-            ++l;
-            continue;
+    LeanTask<NS> A, Bt;
+    await_chunk((lvl[1] - 1 >= 0 ? lvl[1] - 1 : 0) >> lgch);
+    load_task(A, lo + slot, lo + slot < hi);
+    // segments (host plan, analysis.cpp): await the chunks the segment's
+    // lookahead reads, then run its levels in pairs; chunks are released
+    // level by level (predicated arrive, step 6)
+    const bool prof = T.prof != nullptr && threadIdx.x == 0;
+    long long p_wait = 0, p_run = 0, tp = prof ? clock64() : 0;
+    for (int s = 0; s < T.lean_nseg; ++s) {
+        const int4 sg = seg[s];
+        await_chunk(sg.w);
+        if (prof) {
+            const long long tq = clock64();
+            p_wait += tq - tp;
+            tp = tq;
         }
-        for (; l < lend; l += 2) {
+        int l = sg.x;
+        for (; l + 1 < sg.y; l += 2) {
             level(l, A, Bt);
             level(l + 1, Bt, A);
         }
+        if (l < sg.y) level(l, A, Bt);  // the last level when nlev is odd
+        if (prof) {
+            const long long tq = clock64();
+            p_run += tq - tp;
+            tp = tq;
+        }
+    }
+    if (prof) {
+        T.prof[0] = p_wait;
+        T.prof[1] = p_run;
+        T.prof[2] = T.lean_nseg;
+        T.prof[5] = nlev;
     }
 }
 
@@ -330,7 +342,7 @@ int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x
         set_error("no lean triangular kernel for mode %d, n %d", T.mode, T.lean_n);
         return RSB_ESTATE;
     }
-    const size_t smem = (size_t)lean_smem_bytes(T.stage_ch, T.stage_emax, T.diag != nullptr, T.nlevels);
+    const size_t smem = (size_t)lean_dyn_smem_bytes(T.stage_ch, (T.lean_n + 3) & ~3, T.diag != nullptr, T.nlevels);
     k<<<1, kLeanThreads, smem, ctx->stream>>>(v, x, g);
     return RSB_OK;
 }
