@@ -83,21 +83,16 @@ __device__ __forceinline__ int4 lds_v4(unsigned a) {
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+__device__ __forceinline__ void sts_f64_if(bool p, unsigned a, double v) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}" ::"r"(a), "d"(v),
+                 "r"((int)p)
+                 : "memory");
+}
 __device__ __forceinline__ double2 lds_v2f64(unsigned a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
     return v;
 }
-// acc - p unless x == 0 (the entry is skipped: sc.py:261-262 adds nothing
-// for a zero unknown), as one predicated subtraction; NaN is not zero
-// (unordered compare, as C's x != 0)
-__device__ __forceinline__ double sub_unless_zero(double acc, double p, double x) {
-    asm("{\n .reg .pred q;\n setp.neu.f64 q, %2, 0d0000000000000000;\n @q sub.rn.f64 %0, %0, %1;\n}"
-        : "+d"(acc)
-        : "d"(p), "d"(x));
-    return acc;
-}
-
 template <int MODE, int N>
 __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x, Gate g) {
     if (gated(g)) return;
@@ -181,10 +176,10 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int4 s4 = lds_v4(sa + (q * 128 + lane * 4) * 4);
-            S.src[4 * q] = s4.x;
-            S.src[4 * q + 1] = s4.y;
-            S.src[4 * q + 2] = s4.z;
-            S.src[4 * q + 3] = s4.w;
+            S.src[4 * q] = s4.x + s_ring;  // absolute shared addresses: no add on the chain
+            S.src[4 * q + 1] = s4.y + s_ring;
+            S.src[4 * q + 2] = s4.z + s_ring;
+            S.src[4 * q + 3] = s4.w + s_ring;
         }
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -201,7 +196,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         // 1. this level's dependency loads (the only loads on the chain)
         double xv[N];
 #pragma unroll
-        for (int q = 0; q < N; ++q) xv[q] = lds_f64(s_ring + (unsigned)C.src[q]);
+        for (int q = 0; q < N; ++q) xv[q] = lds_f64((unsigned)C.src[q]);
         // 2. the next level's task (independent of this level's values)
         load_task(Nx, hi + slot, hi + slot < hi1);
         // 3. the ordered chain (sc.py:261-262 sequential axpy order, or the
@@ -209,8 +204,13 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         //    read the zero slot and change nothing
         double acc = C.acc;
         if (!(MODE & 1)) {
+            // products off the chain; a skipped entry subtracts +0, which
+            // leaves every acc unchanged (also -0 and NaN)
+            double pr[N];
 #pragma unroll
-            for (int q = 0; q < N; ++q) acc = sub_unless_zero(acc, __dmul_rn(C.v[q], xv[q]), xv[q]);
+            for (int q = 0; q < N; ++q) pr[q] = xv[q] != 0.0 ? __dmul_rn(C.v[q], xv[q]) : 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) acc = __dsub_rn(acc, pr[q]);
         } else {
             double dot = 0.0;
 #pragma unroll
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
             if (C.row >= 0) acc = res;
         }
         // 5. publish
-        if (C.row != -2) ring[(t & (kRing - 1))] = acc;
+        sts_f64_if(C.row != -2, s_ring + (unsigned)(t & (kRing - 1)) * 8, acc);
         stg_f64_if(C.row >= 0, x + (C.row >= 0 ? C.row : 0), acc);
         // 6. a chunk that ends inside this level is done with (its loads were
         //    consumed by this level's chain)
