@@ -35,6 +35,8 @@
 //     copied between registers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device_common.cuh"
 #include "rsb_internal.h"
 
@@ -42,9 +44,11 @@ namespace rsb {
 
 namespace {
 
-constexpr int kLeanConsumers = 128;  // 4 consumer warps, one 32-position slice each per level
+// W consumer warps (one 32-position slice each per level, W = widest level / 32)
+// and one producer warp: warp W, or warp 3 when W = 4 (the rarely used 4th
+// slice then runs on warp 4, sharing SMSP 0 instead of the busiest slice)
+constexpr int kLeanConsumers = 128;
 constexpr int kLeanThreads = kLeanConsumers + 32;
-constexpr int kLeanProducerWarp = 3;  // SMSP 3; the rarely used 4th slice runs on warp 4
 static_assert(kLeanMaxWidth == kLeanConsumers, "one task per consumer thread and level");
 
 // predicated global store (no branch)
@@ -83,6 +87,17 @@ __device__ __forceinline__ int4 lds_v4(unsigned a) {
     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+// four ring offsets, rebased to absolute shared addresses inside the asm (the
+// compiler cannot sink the adds back onto the loads that use them)
+__device__ __forceinline__ int4 lds_v4_rebase(unsigned a, unsigned base) {
+    int4 v;
+    asm volatile(
+        "{\n ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];\n add.s32 %0, %0, %5;\n add.s32 %1, %1, %5;\n"
+        " add.s32 %2, %2, %5;\n add.s32 %3, %3, %5;\n}"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "r"(a), "r"(base));
+    return v;
+}
 __device__ __forceinline__ void sts_f64_if(bool p, unsigned a, double v) {
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}" ::"r"(a), "d"(v),
                  "r"((int)p)
@@ -119,13 +134,16 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         ring[kRing] = 0.0;
         for (int b = 0; b < kStageBufs; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&empty[b], kLeanConsumers / 32);
+            mbar_init(&empty[b], (blockDim.x >> 5) - 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == kLeanProducerWarp) {
+    const int nwarps = (int)(blockDim.x >> 5) - 1;   // consumer warps
+    const int pwarp = nwarps == 4 ? 3 : nwarps;       // producer warp
+    const unsigned nthreads = (unsigned)nwarps * 32;  // consumer threads (named barrier)
+    if (warp == pwarp) {
         // chunk c goes to buffer c % kStageBufs once the consumers released
         // the chunk that held it
         if (lane == 0) {
@@ -146,15 +164,16 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         }
         return;
     }
-    const int slot = warp < kLeanProducerWarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
+    const int slot = warp < pwarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
     // shared-window bases, opaque so they stay in registers (not
     // rematerialised from SR_CgaCtaId every level)
     unsigned s_ring, s_bufs, s_empty;
     asm volatile("mov.u32 %0, %1;" : "=r"(s_ring) : "r"(smem_u32(ring)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_bufs) : "r"(smem_u32(bufs)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_empty) : "r"(smem_u32(empty)));
-    unsigned s_zsrc;
+    unsigned s_zsrc, s_lvl;
     asm volatile("mov.u32 %0, %1;" : "=r"(s_zsrc) : "r"(smem_u32(zsrc)));
+    asm volatile("mov.u32 %0, %1;" : "=r"(s_lvl) : "r"(smem_u32(lvl)));
     int ready = -1;
     auto await_chunk = [&](int c) {
         for (; ready < c;) {
@@ -175,11 +194,11 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         const unsigned sa = has ? B + o_src + base * 4 : s_zsrc;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            const int4 s4 = lds_v4(sa + (q * 128 + lane * 4) * 4);
-            S.src[4 * q] = s4.x + s_ring;  // absolute shared addresses: no add on the chain
-            S.src[4 * q + 1] = s4.y + s_ring;
-            S.src[4 * q + 2] = s4.z + s_ring;
-            S.src[4 * q + 3] = s4.w + s_ring;
+            const int4 s4 = lds_v4_rebase(sa + (q * 128 + lane * 4) * 4, s_ring);  // no add on the chain
+            S.src[4 * q] = s4.x;
+            S.src[4 * q + 1] = s4.y;
+            S.src[4 * q + 2] = s4.z;
+            S.src[4 * q + 3] = s4.w;
         }
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -191,7 +210,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
 
     int lo = lvl[0], hi = lvl[1];
     auto level = [&](int l, LeanTask<NS> &C, LeanTask<NS> &Nx) {
-        const int hi1 = lvl[l + 2];  // end of level l + 1
+        const int hi1 = lds_s32(s_lvl + (unsigned)(l + 2) * 4);  // end of level l + 1
         const int t = lo + slot;
         // 1. this level's dependency loads (the only loads on the chain)
         double xv[N];
@@ -245,7 +264,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
                          "r"((int)cross)
                          : "memory");
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kLeanConsumers) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
         lo = hi;
         hi = hi1;
     };
@@ -343,7 +362,8 @@ int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x
         return RSB_ESTATE;
     }
     const size_t smem = (size_t)lean_dyn_smem_bytes(T.stage_ch, (T.lean_n + 3) & ~3, T.diag != nullptr, T.nlevels);
-    k<<<1, kLeanThreads, smem, ctx->stream>>>(v, x, g);
+    const int warps = (int)std::min<int64_t>(4, std::max<int64_t>(1, (T.max_width + 31) / 32));
+    k<<<1, 32 * (warps + 1), smem, ctx->stream>>>(v, x, g);
     return RSB_OK;
 }
 
