@@ -240,7 +240,8 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
                 em = std::max<int64_t>(128, em);
                 const int64_t lslots = (lean_n + 3) & ~3;  // lean: uniform entry slots per task
                 if (lean_n) em = cand * lslots;
-                const int64_t bytes = lean_n ? lean_dyn_smem_bytes(cand, lslots, !unit, nlev) + kLeanRingBytes
+                const int64_t bytes = lean_n ? lean_dyn_smem_bytes(cand, lslots, !unit, nlev, (ns + cand - 1) / cand) +
+                                                   kLeanRingBytes
                                              : stage_smem_bytes(cand, em, !unit, nlev, (ns + cand - 1) / cand);
                 if (bytes <= kStageSmemBudget) {
                     ch = cand;
@@ -346,38 +347,37 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             }
         }
     }
-    // lean segment plan: the consumers' chunk bookkeeping between runs of
-    // levels (see k_trsv_lean); iteration l prefetches level l + 1, i.e.
-    // reads positions below lvl[l + 2], the level bounds padded with the end
-    std::vector<int4> segs;
+    // lean producer events (k_trsv_lean): chunk c is issued once the level
+    // barriers show that chunk c - kStageBufs is done with (levels below
+    // lvl[j] are, after barrier j - 1), and awaited before barrier j when
+    // iteration j + 1 prefetches from it (positions below lvl[j + 3]);
+    // level -1 is the prologue, before the first barrier
+    std::vector<int2> events;
     if (lean_n) {
         auto L = [&](int64_t i) { return (int64_t)(i <= nlev ? sp[i] : sp[nlev]); };
-        const int64_t nch = nchunks;
-        int64_t released = 0, ready = (std::max<int64_t>(L(1) - 1, 0)) / ch;  // prologue: level 0
-        // chunks awaited beyond the released ones at a segment start (longer
-        // segments against waiting on a chunk still in flight)
-        const int64_t ahead = getenv("RSB_LEAN_AHEAD") ? atoll(getenv("RSB_LEAN_AHEAD")) : kStageBufs - 2;
-        int64_t l = 0;
-        while (l < nlev) {
-            released = std::max(released, L(l) / ch);  // released level by level in the kernel
-            const int64_t need = (L(l + 3) - 1) / ch;  // iterations l, l+1 prefetch levels l+1, l+2
-            // also the chunks issued a segment ago (landed by now), for longer segments
-            int64_t a = std::max(need, std::min(released + ahead, nch - 1));
-            a = std::min(a, released + kStageBufs - 1);
-            ready = std::max(ready, a);
-            const int64_t ready_end = (ready + 1) * ch;
-            int64_t lend = l;
-            while (lend + 2 <= nlev && L(lend + 3) <= ready_end) lend += 2;
-            if (lend == l) lend = l + 1;  // the last level (nlev odd)
-            segs.push_back(make_int4((int)l, (int)lend, (int)released, (int)ready));
-            l = lend;
+        std::vector<int64_t> iss(nchunks, -1), wt(nchunks, -1);
+        for (int64_t c = 0, j = 0; c < nchunks; ++c) {
+            if (c < kStageBufs) continue;
+            while (j < nlev && L(j) / ch + kStageBufs - 1 < c) ++j;
+            iss[c] = j;
         }
+        for (int64_t c = 0, j = 0; c < nchunks; ++c) {
+            if (c <= (std::max<int64_t>(L(2), 1) - 1) / ch) continue;
+            while (j < nlev && (L(j + 3) - 1) / ch < c) ++j;
+            wt[c] = j;
+        }
+        // both are non-decreasing in c: merge by level, issues first
+        for (int64_t j = -1, ci = 0, cw = 0; j < nlev; ++j) {
+            for (; ci < nchunks && iss[ci] == j; ++ci) events.push_back(make_int2((int)j, (int)ci));
+            for (; cw < nchunks && wt[cw] == j; ++cw) events.push_back(make_int2((int)j, (int)(-cw - 1)));
+        }
+        events.push_back(make_int2((int)nlev + 1, 0));  // sentinel
     }
     if (getenv("RSB_DEBUG_ANALYSIS"))
         fprintf(stderr, "[rsb] tri kind=%d n=%lld levels=%d maxw=%lld single_cta=%d lean_n=%d far=%lld ch=%lld emax=%lld "
-                "segments=%zu\n",
+                "\n",
                 kind, (long long)n, nlev, (long long)maxw, (int)single_cta, lean_n, (long long)far, (long long)ch,
-                (long long)emax, segs.size());
+                (long long)emax);
     std::vector<int32_t> rows(order.begin(), order.end());
     rows.resize(padded, 0);
     if (single_cta) rows = srows;  // the staged kernel's gather uses staged positions
@@ -399,11 +399,11 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     S->padded_n = padded;
     S->nrecs = (int64_t)(lean_n ? rval.size() : recs.size());
     if (lean_n) S->stage_emax = (int32_t)(ch * lslots);
+    S->lean_nev = (int32_t)events.size();
     S->lean_n = lean_n;
-    S->lean_nseg = (int32_t)segs.size();
     int rc = RSB_OK;
     if (S->single_cta &&
-        (rc = lean_n ? prepare_trsv_lean(lean_dyn_smem_bytes(ch, lslots, !unit, nlev))
+        (rc = lean_n ? prepare_trsv_lean(lean_dyn_smem_bytes(ch, lslots, !unit, nlev, nchunks))
                      : prepare_trsv_cta((int64_t)stage_smem_bytes(ch, emax, !unit, nlev, nchunks))) != RSB_OK) {
         delete S;
         return rc;
@@ -421,7 +421,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (single_cta && !lean_n && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rval, rval.data(), rval.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rsrc, rsrc.data(), rsrc.size())) != RSB_OK) ||
-        (lean_n && (rc = dev_upload(ctx, &S->lean_seg, segs.data(), segs.size())) != RSB_OK) ||
+        (lean_n && (rc = dev_upload(ctx, &S->lean_ev, events.data(), events.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
@@ -455,7 +455,7 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));
     if (s->rval) dev_free(ctx, s->rval, s->nrecs * sizeof(double));
     if (s->rsrc) dev_free(ctx, s->rsrc, s->nrecs * sizeof(int32_t));
-    if (s->lean_seg) dev_free(ctx, s->lean_seg, s->lean_nseg * sizeof(int4));
+    if (s->lean_ev) dev_free(ctx, s->lean_ev, s->lean_nev * sizeof(int2));
     if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
     if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
     if (s->prof) dev_free(ctx, s->prof, 8 * sizeof(long long));

@@ -73,13 +73,12 @@ struct alignas(16) StageRec {
 inline int64_t lean_buf_bytes(int64_t ch, int64_t ns, bool diag) {
     return ch * (8 + 4 + (diag ? 16 : 0) + ns * 12);
 }
-// upper bound of the lean solve's segment count (segments cover >= 2 levels but the last)
-inline int64_t lean_max_segments(int64_t nlevels) { return nlevels / 2 + 2; }
 // dynamic shared memory: staging buffers, mbarriers, level bounds (nlevels + 5,
-// padded to 4), segment plan; the value ring is a static array
-inline int64_t lean_dyn_smem_bytes(int64_t ch, int64_t ns, bool diag, int64_t nlevels) {
+// padded to 4), the producer's event list (2 per chunk + a sentinel); the
+// value ring is a static array
+inline int64_t lean_dyn_smem_bytes(int64_t ch, int64_t ns, bool diag, int64_t nlevels, int64_t nchunks) {
     return kStageBufs * lean_buf_bytes(ch, ns, diag) + 2 * kStageBufs * 8 + ((nlevels + 8) & ~3LL) * 4 +
-           lean_max_segments(nlevels) * 16;
+           (2 * nchunks + 2) * 8;
 }
 constexpr int64_t kLeanRingBytes = (int64_t)(kRing + 2) * 8;  // ring + a zero slot (+ pad)
 inline int64_t stage_smem_bytes(int64_t ch, int64_t emax, bool diag, int64_t nlevels, int64_t nchunks) {
@@ -159,10 +158,10 @@ struct TriDev {
     // lane quads per 32-position slice (one 16-byte load per 2 / 4 entries)
     const double *rval;
     const int32_t *rsrc;
-    // segment plan {first level, end level, released chunks (info), await chunk}
-    const int4 *lean_seg;
-    int32_t lean_nseg;
     int32_t stage_lgch;  // log2(stage_ch)
+    // lean producer events {level, chunk (issue) or -(chunk + 1) (await)}, by level
+    const int2 *lean_ev;
+    int32_t lean_nev;
     const StageMeta *meta;      // per position (padded to nchunks * stage_ch)
     const double *ddiag;        // per position: {diag, RN(1/diag)} (staged solve's exact division)
     long long *prof;            // optional per-phase cycle counters (RSB_TRSV_PROFILE), else null
@@ -207,8 +206,8 @@ struct TriSched {
     int32_t lean_n = 0;
     double *rval = nullptr;
     int32_t *rsrc = nullptr;
-    int4 *lean_seg = nullptr;
-    int32_t lean_nseg = 0;
+    int2 *lean_ev = nullptr;
+    int32_t lean_nev = 0;
     StageMeta *meta = nullptr;
     double *ddiag = nullptr;
     long long *prof = nullptr;  // 8 counters, allocated when RSB_TRSV_PROFILE is set
@@ -220,7 +219,7 @@ struct TriSched {
     TriDev view() const {
         return TriDev{n,       mode,       task_row, slice_off,  ecol, eval, diag,   ticket,
                       has_far, (int32_t)nlevels,     level_ptr, stage_ch, stage_emax, nchunks,
-                      chunk_roff, bpos,    recs,     rval,       rsrc,  lean_seg, lean_nseg, lgch(), meta, ddiag, prof};
+                      chunk_roff, bpos,    recs,     rval,       rsrc,  lgch(), lean_ev, lean_nev, meta, ddiag, prof};
     }
 };
 

@@ -27,10 +27,12 @@
 //   - the division is Markstein's exact reciprocal division, branch-free;
 //     the rare operand outside its range (zero excepted) takes IEEE division
 //     behind one warp vote;
-//   - task data arrives by 1-D TMA bulk copies into kStageBufs chunk buffers
-//     (producer warp); a consumer warp releases a chunk with a predicated
-//     arrive in the level where it is used up, and awaits chunks only
-//     between segments of levels that the resident chunks cover (host plan);
+//   - task data arrives by 1-D TMA bulk copies into kStageBufs chunk buffers,
+//     issued by a producer warp that takes part in the level barrier: it
+//     lets the consumers into a level only once the chunks that level
+//     prefetches from have landed, and refills a buffer as soon as the
+//     barriers show its chunk is done with -- the consumers never wait on
+//     an mbarrier or release a buffer;
 //   - two task buffers alternate (level loop unrolled by two), so nothing is
 //     copied between registers.
 #include <cuda_runtime.h>
@@ -122,68 +124,76 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
                    o_val = o_dd + (kDiag ? (unsigned)CH * 16 : 0u), o_src = o_val + (unsigned)CH * NS * 8,
                    bb = o_src + (unsigned)CH * NS * 4;
     unsigned long long *full = reinterpret_cast<unsigned long long *>(bufs + kStageBufs * (size_t)bb);
-    unsigned long long *empty = full + kStageBufs;
-    int *lvl = reinterpret_cast<int *>(empty + kStageBufs);
-    const int nlev = T.nlevels, nch = T.nchunks;
-    int4 *seg = reinterpret_cast<int4 *>(lvl + ((nlev + 8) & ~3));
-    // level bounds, padded with the end so lvl[l + 2] is always valid
+    int *lvl = reinterpret_cast<int *>(full + 2 * kStageBufs);
+    const int nlev = T.nlevels;
+    int2 *ev = reinterpret_cast<int2 *>(lvl + ((nlev + 8) & ~3));
+    // level bounds, padded with the end so lvl[l + 3] is always valid
     for (int i = threadIdx.x; i <= nlev + 4; i += blockDim.x) lvl[i] = T.level_ptr[i < nlev ? i : nlev];
-    for (int i = threadIdx.x; i < T.lean_nseg; i += blockDim.x) seg[i] = T.lean_seg[i];
     for (int i = threadIdx.x; i < NS * 32; i += blockDim.x) zsrc[i] = kRing * 8;
+    for (int i = threadIdx.x; i < T.lean_nev; i += blockDim.x) ev[i] = T.lean_ev[i];
     if (threadIdx.x == 0) {
         ring[kRing] = 0.0;
-        for (int b = 0; b < kStageBufs; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&empty[b], (blockDim.x >> 5) - 1);
-        }
+        for (int b = 0; b < kStageBufs; ++b) mbar_init(&full[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = (int)(blockDim.x >> 5) - 1;   // consumer warps
-    const int pwarp = nwarps == 4 ? 3 : nwarps;       // producer warp
-    const unsigned nthreads = (unsigned)nwarps * 32;  // consumer threads (named barrier)
+    const int nwarps = (int)(blockDim.x >> 5) - 1;  // consumer warps
+    const int pwarp = nwarps == 4 ? 3 : nwarps;      // producer warp
+    const unsigned nthreads = blockDim.x;            // the level barrier: consumers + producer
     if (warp == pwarp) {
-        // chunk c goes to buffer c % kStageBufs once the consumers released
-        // the chunk that held it
-        if (lane == 0) {
-            const unsigned bytes = bb;
-            for (int c = 0; c < nch; ++c) {
+        // Producer, in lockstep with the consumers' level barriers: it passes
+        // barrier j only once the chunks that iteration j + 1 prefetches from
+        // have landed, and refills a buffer as soon as the barriers show that
+        // its chunk is done with -- the consumers never touch a chunk-level
+        // barrier.  What to do before which barrier is the host's event list
+        // (analysis.cpp), so a level without events costs a compare.
+        auto issue = [&](int c) {
+            if (lane == 0) {
                 const int b = c & (kStageBufs - 1);
-                if (c >= kStageBufs) mbar_wait_spin(&empty[b], (unsigned)(((c / kStageBufs) - 1) & 1));
                 unsigned char *B = bufs + (size_t)b * bb;
                 const int64_t p0 = (int64_t)c * CH;
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&full[b], bytes);
+                mbar_expect_tx(&full[b], bb);
                 bulk_g2s(B, T.bpos + p0, CH * 8, &full[b]);
                 bulk_g2s(B + o_row, T.task_row + p0, CH * 4, &full[b]);
                 if (kDiag) bulk_g2s(B + o_dd, T.ddiag + 2 * p0, CH * 16, &full[b]);
                 bulk_g2s(B + o_val, T.rval + p0 * NS, (unsigned)CH * NS * 8, &full[b]);
                 bulk_g2s(B + o_src, T.rsrc + p0 * NS, (unsigned)CH * NS * 4, &full[b]);
             }
+        };
+        int e = 0;
+        int2 cur = ev[0];
+        auto events_at = [&](int j) {
+            while (cur.x == j) {
+                if (cur.y >= 0) {
+                    issue(cur.y);
+                } else {
+                    const int c = -cur.y - 1;
+                    mbar_wait_spin(&full[c & (kStageBufs - 1)], (unsigned)((c / kStageBufs) & 1));
+                }
+                cur = ev[++e];
+            }
+        };
+        events_at(-1);  // the first buffers; levels 0 and 1 landed
+        asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+        for (int j = 0; j < nlev; ++j) {
+            events_at(j);
+            asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
         }
         return;
     }
     const int slot = warp < pwarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
     // shared-window bases, opaque so they stay in registers (not
     // rematerialised from SR_CgaCtaId every level)
-    unsigned s_ring, s_bufs, s_empty;
+    unsigned s_ring, s_bufs, s_zsrc, s_lvl;
     asm volatile("mov.u32 %0, %1;" : "=r"(s_ring) : "r"(smem_u32(ring)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_bufs) : "r"(smem_u32(bufs)));
-    asm volatile("mov.u32 %0, %1;" : "=r"(s_empty) : "r"(smem_u32(empty)));
-    unsigned s_zsrc, s_lvl;
     asm volatile("mov.u32 %0, %1;" : "=r"(s_zsrc) : "r"(smem_u32(zsrc)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_lvl) : "r"(smem_u32(lvl)));
-    int ready = -1;
-    auto await_chunk = [&](int c) {
-        for (; ready < c;) {
-            ++ready;
-            mbar_wait_spin(&full[ready & (kStageBufs - 1)], (unsigned)((ready / kStageBufs) & 1));
-        }
-    };
     // all of the task at position t, unconditionally; a lane without a task
-    // (a position past the level, possibly in a chunk not yet landed) reads
-    // its sources from zsrc, the rest is loaded and never published
+    // (a position past the level) reads its sources from zsrc, the rest is
+    // loaded and never published
     auto load_task = [&](LeanTask<NS> &S, int t, bool has) {
         const unsigned B = s_bufs + (unsigned)((t >> lgch) & (kStageBufs - 1)) * bb;
         const unsigned loc = (unsigned)(t & (CH - 1)), base = (loc - (unsigned)lane) * NS;
@@ -209,6 +219,8 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     };
 
     int lo = lvl[0], hi = lvl[1];
+    const bool cprof = T.prof != nullptr && threadIdx.x == 0;
+    long long cbusy = 0, ct0 = 0;
     auto level = [&](int l, LeanTask<NS> &C, LeanTask<NS> &Nx) {
         const int hi1 = lds_s32(s_lvl + (unsigned)(l + 2) * 4);  // end of level l + 1
         const int t = lo + slot;
@@ -254,53 +266,31 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         // 5. publish
         sts_f64_if(C.row != -2, s_ring + (unsigned)(t & (kRing - 1)) * 8, acc);
         stg_f64_if(C.row >= 0, x + (C.row >= 0 ? C.row : 0), acc);
-        // 6. a chunk that ends inside this level is done with (its loads were
-        //    consumed by this level's chain)
-        {
-            const int c0 = lo >> lgch;
-            const bool cross = lane == 0 && (hi >> lgch) != c0;
-            asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %1, 0;\n @p mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(
-                             s_empty + (unsigned)(c0 & (kStageBufs - 1)) * 8),
-                         "r"((int)cross)
-                         : "memory");
-        }
+        if (cprof) cbusy += clock64() - ct0;
         asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+        if (cprof) ct0 = clock64();
         lo = hi;
         hi = hi1;
     };
 
     LeanTask<NS> A, Bt;
-    await_chunk((lvl[1] - 1 >= 0 ? lvl[1] - 1 : 0) >> lgch);
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // levels 0 and 1 have landed
     load_task(A, lo + slot, lo + slot < hi);
-    // segments (host plan, analysis.cpp): await the chunks the segment's
-    // lookahead reads, then run its levels in pairs; chunks are released
-    // level by level (predicated arrive, step 6)
+    if (cprof) ct0 = clock64();
     const bool prof = T.prof != nullptr && threadIdx.x == 0;
-    long long p_wait = 0, p_run = 0, tp = prof ? clock64() : 0;
-    for (int s = 0; s < T.lean_nseg; ++s) {
-        const int4 sg = seg[s];
-        await_chunk(sg.w);
-        if (prof) {
-            const long long tq = clock64();
-            p_wait += tq - tp;
-            tp = tq;
-        }
-        int l = sg.x;
-        for (; l + 1 < sg.y; l += 2) {
-            level(l, A, Bt);
-            level(l + 1, Bt, A);
-        }
-        if (l < sg.y) level(l, A, Bt);  // the last level when nlev is odd
-        if (prof) {
-            const long long tq = clock64();
-            p_run += tq - tp;
-            tp = tq;
-        }
+    const long long tp = prof ? clock64() : 0;
+    int l = 0;
+    for (; l + 1 < nlev; l += 2) {
+        level(l, A, Bt);
+        level(l + 1, Bt, A);
     }
+    if (l < nlev) level(l, A, Bt);  // the last level when nlev is odd
     if (prof) {
-        T.prof[0] = p_wait;
-        T.prof[1] = p_run;
-        T.prof[2] = T.lean_nseg;
+        T.prof[0] = cbusy;
+        T.prof[1] = clock64() - tp;
+        T.prof[2] = 1;
+        T.prof[3] = 0;
+        T.prof[4] = T.nchunks;
         T.prof[5] = nlev;
     }
 }
@@ -361,7 +351,8 @@ int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x
         set_error("no lean triangular kernel for mode %d, n %d", T.mode, T.lean_n);
         return RSB_ESTATE;
     }
-    const size_t smem = (size_t)lean_dyn_smem_bytes(T.stage_ch, (T.lean_n + 3) & ~3, T.diag != nullptr, T.nlevels);
+    const size_t smem =
+        (size_t)lean_dyn_smem_bytes(T.stage_ch, (T.lean_n + 3) & ~3, T.diag != nullptr, T.nlevels, T.nchunks);
     const int warps = (int)std::min<int64_t>(4, std::max<int64_t>(1, (T.max_width + 31) / 32));
     k<<<1, 32 * (warps + 1), smem, ctx->stream>>>(v, x, g);
     return RSB_OK;
