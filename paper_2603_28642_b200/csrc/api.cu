@@ -383,6 +383,15 @@ int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters) {
     return RSB_OK;
 }
 
+int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n) {
+    TriSched *S = nullptr;
+    RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
+    RSB_TRY(get_tri(T, kind, &S));
+    *variant = S->lean_n ? RSB_TRSV_LEAN : (S->single_cta ? RSB_TRSV_STAGED : RSB_TRSV_GRID);
+    *lean_n = S->lean_n;
+    return RSB_OK;
+}
+
 int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width) {
     TriSched *S = nullptr;
     RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
