@@ -313,6 +313,8 @@ def run_b200(args):
     solver = device_solver(dA, dpre)
     lv_l1 = dpre.L1.levels(L.TRI_LOWER_UNIT)
     lv_u = dpre.U.levels(L.TRI_UPPER)
+    variants = {"L1": dpre.L1.variant(L.TRI_LOWER_UNIT), "L1T": dpre.L1.variant(L.TRI_LOWER_T_UNIT),
+                "U": dpre.U.variant(L.TRI_UPPER)}
     times["upload_and_analysis_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     norm_a = P.power_method_norm2(S, 100, args.config)
@@ -420,8 +422,8 @@ def run_b200(args):
             "dot_order": "exact (reference OpenBLAS association)",
         },
         "roofline": {
-            "kernel": "k_trsv_stage (+ k_gather_pos): level-synchronous single-CTA triangular solves, "
-                      "8 per cg(2) iteration",
+            "kernel": "triangular solves (+ k_gather_pos), 8 per cg(2) iteration: "
+                      + ", ".join(f"{k}: k_trsv_{v[0]}" + (f"<N={v[1]}>" if v[1] else "") for k, v in variants.items()),
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
             "traffic_source": traffic_src,
