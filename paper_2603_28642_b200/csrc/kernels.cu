@@ -19,8 +19,8 @@ constexpr int kBlock = 256;
 constexpr int kTriBlock = 128;
 constexpr int kCtaTri = 128;
 constexpr int kStageRegs = 16;
-constexpr int kDotChunk = 2048;  // elements per vector per stage of the staged exact dot
-constexpr int kDotStages = 3;  // entries per task held in registers by the staged solve
+constexpr int kDotChunk = 6144;  // elements per vector per stage of the staged exact dot (48 KB copies)
+constexpr int kDotStages = 2;  // stages (a bulk copy occupies the SM's TMA ~900 cycles at any size up to 64 KB: few, large copies)
 
 
 __device__ __forceinline__ double vin(const VecIn &v, int64_t i) {
@@ -452,11 +452,39 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double
     double acc = 0.0;
     for (int64_t c = 0; c < nch; ++c) {
         const int st = (int)(c % kDotStages);
-        mbar_wait(&bar[st], (unsigned)((c / kDotStages) & 1));
-        const double *sa = dbuf + (size_t)st * 2 * kDotChunk, *sb = sa + kDotChunk;
-        const int cnt = (int)min((int64_t)kDotChunk, n32 - c * kDotChunk);
-#pragma unroll 8
-        for (int i = lane; i < cnt; i += 32) acc = fma(sa[i], sb[i], acc);
+        mbar_wait_spin(&bar[st], (unsigned)((c / kDotStages) & 1));
+        const double *sa = dbuf + (size_t)st * 2 * kDotChunk + lane, *sb = sa + kDotChunk;
+        const int steps = (int)min((int64_t)kDotChunk, n32 - c * kDotChunk) / 32;
+        // the lane's FMA chain, 8 cycles a step: operands of the next 8 steps
+        // are loaded while the current 8 issue, so the chain never waits on
+        // shared-memory latency
+        constexpr int G = 8;
+        const int full_groups = steps / G;
+        double ra[G], rb[G];
+        if (full_groups > 0) {
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                ra[j] = sa[32 * j];
+                rb[j] = sb[32 * j];
+            }
+        }
+        for (int gI = 0; gI < full_groups; ++gI) {
+            double na[G], nb[G];
+            const int nxt = (gI + 1 < full_groups) ? (gI + 1) * G : gI * G;  // last group: reload, unused
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                na[j] = sa[32 * (nxt + j)];
+                nb[j] = sb[32 * (nxt + j)];
+            }
+#pragma unroll
+            for (int j = 0; j < G; ++j) acc = fma(ra[j], rb[j], acc);
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                ra[j] = na[j];
+                rb[j] = nb[j];
+            }
+        }
+        for (int k = full_groups * G; k < steps; ++k) acc = fma(sa[32 * k], sb[32 * k], acc);
         __syncwarp();
         if (lane == 0 && c + kDotStages < nch) issue(c + kDotStages);
     }

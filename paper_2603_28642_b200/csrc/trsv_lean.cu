@@ -164,13 +164,16 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         };
         int e = 0;
         int2 cur = ev[0];
+        long long pwait = 0;
         auto events_at = [&](int j) {
             while (cur.x == j) {
                 if (cur.y >= 0) {
                     issue(cur.y);
                 } else {
                     const int c = -cur.y - 1;
+                    const long long tw = T.prof ? clock64() : 0;
                     mbar_wait_spin(&full[c & (kStageBufs - 1)], (unsigned)((c / kStageBufs) & 1));
+                    if (T.prof) pwait += clock64() - tw;
                 }
                 cur = ev[++e];
             }
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
             events_at(j);
             asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
         }
+        if (T.prof && lane == 0) T.prof[6] = pwait;
         return;
     }
     const int slot = warp < pwarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
