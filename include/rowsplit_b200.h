@@ -110,12 +110,15 @@ int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where);
 int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters);
 /* dependency levels of the (matrix, kind) solve DAG (analysing it if needed) */
 int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
-/* which kernel runs the (matrix, kind) solve: RSB_TRSV_GRID (grid-wide,
- * wide DAGs), RSB_TRSV_STAGED (one CTA, staged records) or RSB_TRSV_LEAN (one
- * CTA, register-pipelined; *lean_n = its longest task, else 0) */
+/* which kernel runs the (matrix, kind) solve: RSB_TRSV_GRID (sync-free
+ * grid-wide, wide DAGs), RSB_TRSV_STAGED (one CTA, staged records),
+ * RSB_TRSV_LEAN (one CTA, register-pipelined; *lean_n = its longest task,
+ * else 0) or RSB_TRSV_LEVELS (a grid launch per level: wide DAGs with few
+ * levels) */
 #define RSB_TRSV_GRID 0
 #define RSB_TRSV_STAGED 1
 #define RSB_TRSV_LEAN 2
+#define RSB_TRSV_LEVELS 3
 int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n);
 /* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),
  * drawn by the caller (host RNG stays on the host). */

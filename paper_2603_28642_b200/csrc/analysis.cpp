@@ -410,6 +410,16 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     }
     std::vector<int32_t> lptr(lstart.begin(), lstart.end());
     if (single_cta) lptr.assign(sp.begin(), sp.end());
+    if (!single_cta) {
+        // a grid launch per level is an option (RSB_TRSV_GRID=levels); on
+        // config 4 at mu = 1 (23 / 66 levels) it measured 2x slower than the
+        // sync-free kernel, so it is off by default
+        const char *gv = getenv("RSB_TRSV_GRID");  // "levels" | "syncfree" (experiments)
+        S->level_launch = nlev <= kLevelLaunchMaxLevels;
+        if (gv && std::strcmp(gv, "levels") == 0) S->level_launch = true;
+        if (gv && std::strcmp(gv, "syncfree") == 0) S->level_launch = false;
+        S->h_level_ptr = lptr;
+    }
     if ((rc = dev_upload(ctx, &S->level_ptr, lptr.data(), lptr.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->task_row, rows.data(), rows.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->slice_off, soff.data(), nslices + 1)) != RSB_OK ||

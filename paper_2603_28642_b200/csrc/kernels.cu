@@ -416,6 +416,20 @@ __global__ void __launch_bounds__(kTriBlock) k_trsv(TriDev T, VecIn a, const dou
     }
 }
 
+// Level-synchronous grid solve (wide DAGs with few levels): one launch per
+// level, one thread per task; every dependency was published by an earlier
+// launch, so operands are plain loads and nothing polls.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_trsv_level(TriDev T, VecIn a, const double *c, double *x, int lo, int hi,
+                                                       Gate g) {
+    if (gated(g)) return;
+    for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+        Task k;
+        load_task<MODE>(T, t, a, c, k);
+        x[k.row] = task_value<MODE>(T, k, [&](int j) { return x[j]; });
+    }
+}
+
 __device__ __forceinline__ double canonical(double v) {
     return __double_as_longlong(v) == (long long)kSentinel ? __longlong_as_double(0x7FF8000000000000ll) : v;
 }
@@ -911,6 +925,18 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
             case 5: k_trsv_stage<1, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
             case 6: k_trsv_stage<2, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
             default: k_trsv_stage<3, true><<<1, kCtaTri + 32, smem, ctx->stream>>>(v, x, g); break;
+        }
+    } else if (T.level_launch) {
+        for (int32_t l = 0; l + 1 < (int32_t)T.h_level_ptr.size(); ++l) {
+            const int lo = T.h_level_ptr[l], hi = T.h_level_ptr[l + 1];
+            const int grid = (int)std::min<int64_t>((hi - lo + kBlock - 1) / kBlock, 148 * 16);
+            switch (T.mode) {
+                case 0: k_trsv_level<0><<<grid, kBlock, 0, ctx->stream>>>(v, a, c, x, lo, hi, g); break;
+                case 1: k_trsv_level<1><<<grid, kBlock, 0, ctx->stream>>>(v, a, c, x, lo, hi, g); break;
+                case 2: k_trsv_level<2><<<grid, kBlock, 0, ctx->stream>>>(v, a, c, x, lo, hi, g); break;
+                default: k_trsv_level<3><<<grid, kBlock, 0, ctx->stream>>>(v, a, c, x, lo, hi, g); break;
+            }
+            if (l + 2 < (int32_t)T.h_level_ptr.size()) RSB_TRY(post_launch(ctx));
         }
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));

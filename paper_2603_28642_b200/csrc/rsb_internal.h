@@ -50,6 +50,9 @@ constexpr int kRing = 4096;
 // lean staged solve: widest level (one task per consumer thread) and longest task
 constexpr int64_t kLeanMaxWidth = 128;
 constexpr int64_t kLeanMaxN = 16;
+// grid-wide solves with at most this many levels launch one kernel per level
+// (0: only on request, RSB_TRSV_GRID=levels)
+constexpr int32_t kLevelLaunchMaxLevels = 0;
 constexpr int kStageBufs = 4;
 constexpr int kStageSmemBudget = 220 * 1024;
 // shared-memory bytes of one staging buffer
@@ -204,6 +207,10 @@ struct TriSched {
     // lean variant: every task holds at most lean_n entries, levels are at most
     // kCtaTri wide and no dependency is older than the ring; 0 = not lean
     int32_t lean_n = 0;
+    // wide DAGs with few levels: one grid launch per level instead of the
+    // sync-free grid kernel; host copy of the level bounds
+    bool level_launch = false;
+    std::vector<int32_t> h_level_ptr;
     double *rval = nullptr;
     int32_t *rsrc = nullptr;
     int2 *lean_ev = nullptr;

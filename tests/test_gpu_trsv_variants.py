@@ -4,7 +4,7 @@ Matrices are built level by level so that each case lands on a chosen
 kernel: the lean single-CTA solve (trsv_lean.cu) at every consumer-warp
 count and the longest task it takes (16 entries in the sequential order, 15
 in the dot order), the staged single-CTA solve past those limits, and the
-grid-wide solve for wide DAGs -- with an odd number of levels, many
+grid-wide solves for wide DAGs (a launch per level, or sync-free) -- with an odd number of levels, many
 chunks, diagonals and right-hand sides outside the exact-division range,
 signed zeros, infinities and NaNs.  Every case also runs with the lean
 kernel disabled (RSB_TRSV_LEAN=0) and must give the same bits.
@@ -120,9 +120,15 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
     rng = np.random.default_rng(2)
     M = leveled_lower([160] * 40, 5, rng)
     b = rng.standard_normal(M.ncols)
-    assert check(M, L.TRI_LOWER_UNIT, b, monkeypatch)[0] in ("staged", "grid")
+    assert check(M, L.TRI_LOWER_UNIT, b, monkeypatch)[0] in ("staged", "grid", "levels")
     W = leveled_lower([6000] * 5, 4, rng)
-    assert check(W, L.TRI_LOWER_UNIT, rng.standard_normal(W.ncols), monkeypatch)[0] == "grid"
+    bw = rng.standard_normal(W.ncols)
+    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+    # a grid launch per level on the same DAG
+    with monkeypatch.context() as m:
+        m.setenv("RSB_TRSV_GRID", "levels")
+        W2 = P.CscMatrix(W.nrows, W.ncols, W.col_ptr.copy(), W.row_idx.copy(), W.values.copy())
+        assert check(W2, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levels"
 
 
 def test_many_chunks_every_kind(monkeypatch):
