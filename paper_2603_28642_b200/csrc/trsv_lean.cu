@@ -105,6 +105,55 @@ __device__ __forceinline__ void sts_f64_if(bool p, unsigned a, double v) {
                  "r"((int)p)
                  : "memory");
 }
+// the same with a compile-time byte offset folded into the instruction
+template <int OFF>
+__device__ __forceinline__ int4 lds_v4_rebase_at(unsigned a, unsigned base) {
+    int4 v;
+    asm volatile(
+        "{\n ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+%6];\n add.s32 %0, %0, %5;\n add.s32 %1, %1, %5;\n"
+        " add.s32 %2, %2, %5;\n add.s32 %3, %3, %5;\n}"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "r"(a), "r"(base), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ double2 lds_v2f64_at(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int Q, int NQ_>
+struct SrcQuads {
+    template <class S>
+    __device__ __forceinline__ static void run(S &st, unsigned a, unsigned base) {
+        const int4 s4 = lds_v4_rebase_at<Q * 512>(a, base);
+        st.src[4 * Q] = s4.x;
+        st.src[4 * Q + 1] = s4.y;
+        st.src[4 * Q + 2] = s4.z;
+        st.src[4 * Q + 3] = s4.w;
+        SrcQuads<Q + 1, NQ_>::run(st, a, base);
+    }
+};
+template <int NQ_>
+struct SrcQuads<NQ_, NQ_> {
+    template <class S>
+    __device__ __forceinline__ static void run(S &, unsigned, unsigned) {}
+};
+template <int Q, int NP_>
+struct ValPairs {
+    template <class S>
+    __device__ __forceinline__ static void run(S &st, unsigned a) {
+        const double2 v2 = lds_v2f64_at<Q * 512>(a);
+        st.v[2 * Q] = v2.x;
+        st.v[2 * Q + 1] = v2.y;
+        ValPairs<Q + 1, NP_>::run(st, a);
+    }
+};
+template <int NP_>
+struct ValPairs<NP_, NP_> {
+    template <class S>
+    __device__ __forceinline__ static void run(S &, unsigned) {}
+};
 __device__ __forceinline__ double2 lds_v2f64(unsigned a) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
@@ -205,21 +254,11 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         S.row = has ? row : -2;
         S.acc = lds_f64(B + loc * 8);
         S.dr = kDiag ? lds_v2f64(B + o_dd + loc * 16) : make_double2(1.0, 1.0);
-        const unsigned sa = has ? B + o_src + base * 4 : s_zsrc;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int4 s4 = lds_v4_rebase(sa + (q * 128 + lane * 4) * 4, s_ring);  // no add on the chain
-            S.src[4 * q] = s4.x;
-            S.src[4 * q + 1] = s4.y;
-            S.src[4 * q + 2] = s4.z;
-            S.src[4 * q + 3] = s4.w;
-        }
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const double2 v2 = lds_v2f64(B + o_val + (base + q * 64 + lane * 2) * 8);
-            S.v[2 * q] = v2.x;
-            S.v[2 * q + 1] = v2.y;
-        }
+        // one base address per array, the 16-byte groups at immediate offsets;
+        // sources are rebased to absolute ring addresses (no add on the chain)
+        const unsigned sa = (has ? B + o_src + base * 4 : s_zsrc) + (unsigned)lane * 16;
+        SrcQuads<0, NQ>::run(S, sa, s_ring);
+        ValPairs<0, NP>::run(S, B + o_val + base * 8 + (unsigned)lane * 16);
     };
 
     int lo = lvl[0], hi = lvl[1];
