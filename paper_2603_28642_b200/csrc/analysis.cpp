@@ -410,6 +410,13 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     }
     std::vector<int32_t> lptr(lstart.begin(), lstart.end());
     if (single_cta) lptr.assign(sp.begin(), sp.end());
+    {
+        int64_t ml = 0;
+        for (int64_t t = 0; t < n; ++t) ml = std::max(ml, tptr[t + 1] - tptr[t]);
+        S->max_task = (int32_t)ml;
+        const char *wv = getenv("RSB_TRSV_WIDE");  // "0": the previous grid kernel (experiments)
+        S->wide = !single_cta && !(is_dot && ml >= 16) && !(wv && std::strcmp(wv, "0") == 0);
+    }
     if (!single_cta) {
         // a grid launch per level is an option (RSB_TRSV_GRID=levels); on
         // config 4 at mu = 1 (23 / 66 levels) it measured 2x slower than the
@@ -427,7 +434,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (rc = dev_upload(ctx, &S->eval, eval.data(), slots)) != RSB_OK ||
         (!unit && (rc = dev_upload(ctx, &S->diag, tdiag.data(), tdiag.size())) != RSB_OK) ||
         (single_cta && (rc = dev_upload(ctx, &S->chunk_roff, croff.data(), croff.size())) != RSB_OK) ||
-        (single_cta && (rc = dev_alloc(ctx, (void **)&S->bpos, padded * sizeof(double))) != RSB_OK) ||
+        ((single_cta || S->wide) && (rc = dev_alloc(ctx, (void **)&S->bpos, padded * sizeof(double))) != RSB_OK) ||
         (single_cta && !lean_n && (rc = dev_upload(ctx, &S->recs, recs.data(), recs.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rval, rval.data(), rval.size())) != RSB_OK) ||
         (lean_n && (rc = dev_upload(ctx, &S->rsrc, rsrc.data(), rsrc.size())) != RSB_OK) ||

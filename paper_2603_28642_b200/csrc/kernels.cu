@@ -938,6 +938,12 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
             }
             if (l + 2 < (int32_t)T.h_level_ptr.size()) RSB_TRY(post_launch(ctx));
         }
+    } else if (T.wide) {
+        k_gather_pos<<<grid_stride(T.n), kBlock, 0, ctx->stream>>>(T.n, T.n, T.task_row, a, c, v.bpos, g);
+        RSB_TRY(post_launch(ctx));
+        RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
+        RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
+        RSB_TRY(launch_trsv_wide(ctx, T, v, v.bpos, x, g));
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         // blocks number themselves in start order from this counter

@@ -210,6 +210,10 @@ struct TriSched {
     // wide DAGs with few levels: one grid launch per level instead of the
     // sync-free grid kernel; host copy of the level bounds
     bool level_launch = false;
+    // longest task; the persistent wide kernel (trsv_wide.cu) runs the grid
+    // schedule unless a dot-order task has >= 16 entries (blocked BLAS order)
+    int32_t max_task = 0;
+    bool wide = false;
     std::vector<int32_t> h_level_ptr;
     double *rval = nullptr;
     int32_t *rsrc = nullptr;
@@ -305,6 +309,7 @@ int get_tri(rsb_mat *T, int kind, TriSched **out);
 int prepare_trsv_cta(int64_t n);
 int prepare_trsv_lean(int64_t smem_bytes);
 int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
+int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g);
 // one-time kernel attribute setup for the dense S solve of size s
 int prepare_chol(int64_t s);
 // one-time kernel attribute setup at context creation (dynamic shared memory)
