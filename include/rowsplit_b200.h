@@ -108,6 +108,9 @@ int rsb_trsv(rsb_mat *T, int kind, const double *b, double *x, int where);
 /* diagnostics: per-phase cycle counters of the last staged solve of (matrix,
  * kind); only when the schedule was analysed with RSB_TRSV_PROFILE set */
 int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters);
+/* diagnostics (wide solve, RSB_TRSV_PROFILE): stamps[0] = start, stamps[1 + l]
+ * = %globaltimer when level l completed, for min(cap, 4097) entries */
+int rsb_trsv_profile_levels(rsb_mat *T, int kind, long long *stamps, int64_t cap);
 /* dependency levels of the (matrix, kind) solve DAG (analysing it if needed) */
 int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
 /* which kernel runs the (matrix, kind) solve: RSB_TRSV_GRID (sync-free

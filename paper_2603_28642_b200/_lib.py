@@ -67,6 +67,7 @@ _SIGS = {
     "rsb_trsv": [vp, ctypes.c_int, vp, vp, ctypes.c_int],
     "rsb_trsv_levels": [vp, ctypes.c_int, i64p, i64p],
     "rsb_trsv_variant": [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
+    "rsb_trsv_profile_levels": [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong), i64],
     "rsb_trsv_profile": [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_longlong)],
     "rsb_power_norm2": [vp, vp, ctypes.c_int, f64p],
     "rsb_dot": [vp, i64, vp, vp, f64p, ctypes.c_int],

@@ -442,7 +442,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
-        (getenv("RSB_TRSV_PROFILE") && (rc = dev_alloc(ctx, (void **)&S->prof, 8 * sizeof(long long))) != RSB_OK)) {
+        (getenv("RSB_TRSV_PROFILE") && (rc = dev_alloc(ctx, (void **)&S->prof, (8 + 4096) * sizeof(long long))) != RSB_OK)) {
         tri_free(ctx, S);
         return rc;
     }
@@ -475,7 +475,7 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->lean_ev) dev_free(ctx, s->lean_ev, s->lean_nev * sizeof(int2));
     if (s->meta) dev_free(ctx, s->meta, padded * sizeof(StageMeta));
     if (s->ddiag) dev_free(ctx, s->ddiag, 2 * padded * sizeof(double));
-    if (s->prof) dev_free(ctx, s->prof, 8 * sizeof(long long));
+    if (s->prof) dev_free(ctx, s->prof, (8 + 4096) * sizeof(long long));
     delete s;
 }
 

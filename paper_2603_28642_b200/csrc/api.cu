@@ -383,6 +383,20 @@ int rsb_trsv_profile(rsb_mat *T, int kind, long long *counters) {
     return RSB_OK;
 }
 
+int rsb_trsv_profile_levels(rsb_mat *T, int kind, long long *stamps, int64_t cap) {
+    TriSched *S = nullptr;
+    RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
+    RSB_TRY(get_tri(T, kind, &S));
+    if (!S->prof) {
+        set_error("triangular schedule was analysed without RSB_TRSV_PROFILE");
+        return RSB_ESTATE;
+    }
+    const int64_t k = std::min<int64_t>(cap, 4097);
+    RSB_TRY_CUDA(cudaMemcpyAsync(stamps, S->prof + 7, k * sizeof(long long), cudaMemcpyDeviceToHost, T->ctx->stream));
+    RSB_TRY_CUDA(cudaStreamSynchronize(T->ctx->stream));
+    return RSB_OK;
+}
+
 int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n) {
     TriSched *S = nullptr;
     RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));

@@ -122,11 +122,19 @@ __device__ __forceinline__ double2 lds_v2f64_at(unsigned a) {
     asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(OFF));
     return v;
 }
+template <int OFF>
+__device__ __forceinline__ int4 lds_v4_at(unsigned a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a), "n"(OFF));
+    return v;
+}
 template <int Q, int NQ_>
 struct SrcQuads {
     template <class S>
     __device__ __forceinline__ static void run(S &st, unsigned a, unsigned base) {
-        const int4 s4 = lds_v4_rebase_at<Q * 512>(a, base);
+        const int4 s4 = lds_v4_at<Q * 512>(a);
         st.src[4 * Q] = s4.x;
         st.src[4 * Q + 1] = s4.y;
         st.src[4 * Q + 2] = s4.z;
@@ -238,39 +246,45 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     }
     const int slot = warp < pwarp ? (int)threadIdx.x : (int)threadIdx.x - 32;
     // shared-window bases, opaque so they stay in registers (not
-    // rematerialised from SR_CgaCtaId every level)
+    // rematerialised from SR_CgaCtaId every level); the ring's own base is
+    // left to the compiler, which keeps it in a uniform register
     unsigned s_ring, s_bufs, s_zsrc, s_lvl;
     asm volatile("mov.u32 %0, %1;" : "=r"(s_ring) : "r"(smem_u32(ring)));
+    const unsigned u_ring = smem_u32(ring);
+    auto ring_ld = [&](unsigned off) { return lds_f64(u_ring + off); };
     asm volatile("mov.u32 %0, %1;" : "=r"(s_bufs) : "r"(smem_u32(bufs)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_zsrc) : "r"(smem_u32(zsrc)));
     asm volatile("mov.u32 %0, %1;" : "=r"(s_lvl) : "r"(smem_u32(lvl)));
     // all of the task at position t, unconditionally; a lane without a task
     // (a position past the level) reads its sources from zsrc, the rest is
     // loaded and never published
+    // A lane without a task (a position past the level) points every load at
+    // zsrc with no lane offset: its warp's loads become single-wavefront
+    // broadcasts instead of competing with the busy warps for shared-memory
+    // bandwidth, and its sources are the ring's zero slot.
     auto load_task = [&](LeanTask<NS> &S, int t, bool has) {
         const unsigned B = s_bufs + (unsigned)((t >> lgch) & (kStageBufs - 1)) * bb;
         const unsigned loc = (unsigned)(t & (CH - 1)), base = (loc - (unsigned)lane) * NS;
-        const int row = lds_s32(B + o_row + loc * 4);
+        const int row = lds_s32(has ? B + o_row + loc * 4 : s_zsrc);
         S.row = has ? row : -2;
-        S.acc = lds_f64(B + loc * 8);
-        S.dr = kDiag ? lds_v2f64(B + o_dd + loc * 16) : make_double2(1.0, 1.0);
+        S.acc = lds_f64(has ? B + loc * 8 : s_zsrc);
+        S.dr = kDiag ? lds_v2f64(has ? B + o_dd + loc * 16 : s_zsrc) : make_double2(1.0, 1.0);
         // one base address per array, the 16-byte groups at immediate offsets;
-        // sources are rebased to absolute ring addresses (no add on the chain)
-        const unsigned sa = (has ? B + o_src + base * 4 : s_zsrc) + (unsigned)lane * 16;
+        // sources stay ring offsets: the ring's base is a uniform register
+        // that the ring loads add for free ([R + UR] addressing)
+        const unsigned sa = has ? B + o_src + base * 4 + (unsigned)lane * 16 : s_zsrc;
         SrcQuads<0, NQ>::run(S, sa, s_ring);
-        ValPairs<0, NP>::run(S, B + o_val + base * 8 + (unsigned)lane * 16);
+        ValPairs<0, NP>::run(S, has ? B + o_val + base * 8 + (unsigned)lane * 16 : s_zsrc);
     };
 
     int lo = lvl[0], hi = lvl[1];
-    const bool cprof = T.prof != nullptr && threadIdx.x == 0;
-    long long cbusy = 0, ct0 = 0;
     auto level = [&](int l, LeanTask<NS> &C, LeanTask<NS> &Nx) {
         const int hi1 = lds_s32(s_lvl + (unsigned)(l + 2) * 4);  // end of level l + 1
         const int t = lo + slot;
         // 1. this level's dependency loads (the only loads on the chain)
         double xv[N];
 #pragma unroll
-        for (int q = 0; q < N; ++q) xv[q] = lds_f64((unsigned)C.src[q]);
+        for (int q = 0; q < N; ++q) xv[q] = ring_ld((unsigned)C.src[q]);
         // 2. the next level's task (independent of this level's values)
         load_task(Nx, hi + slot, hi + slot < hi1);
         // 3. the ordered chain (sc.py:261-262 sequential axpy order, or the
@@ -309,9 +323,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
         // 5. publish
         sts_f64_if(C.row != -2, s_ring + (unsigned)(t & (kRing - 1)) * 8, acc);
         stg_f64_if(C.row >= 0, x + (C.row >= 0 ? C.row : 0), acc);
-        if (cprof) cbusy += clock64() - ct0;
         asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-        if (cprof) ct0 = clock64();
         lo = hi;
         hi = hi1;
     };
@@ -319,7 +331,6 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     LeanTask<NS> A, Bt;
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // levels 0 and 1 have landed
     load_task(A, lo + slot, lo + slot < hi);
-    if (cprof) ct0 = clock64();
     const bool prof = T.prof != nullptr && threadIdx.x == 0;
     const long long tp = prof ? clock64() : 0;
     int l = 0;
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     }
     if (l < nlev) level(l, A, Bt);  // the last level when nlev is odd
     if (prof) {
-        T.prof[0] = cbusy;
+        T.prof[0] = 0;
         T.prof[1] = clock64() - tp;
         T.prof[2] = 1;
         T.prof[3] = 0;

@@ -94,6 +94,11 @@ __global__ void __launch_bounds__(kWideBlock) k_trsv_wide(TriDev T, const double
         return __shfl_sync(0xffffffffu, s, 0);
     };
     int s = take();
+    if (T.prof && s == 0 && lane == 0) {  // diagnostics: start stamp
+        unsigned long long ts;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
+        T.prof[7] = (long long)ts;
+    }
     while (s < nslices) {
         const int s_next = take();  // latency overlaps this slice
         const int t = s * 32 + lane;
