@@ -131,6 +131,28 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
         assert check(W2, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levels"
 
 
+@pytest.mark.parametrize("k", [3, 12, 20])
+def test_wide_kernel_every_kind_and_long_tasks(k, monkeypatch):
+    """The persistent wide solve (grid schedules): tasks past its register
+    entries take the out-of-line tail (sequential order) and wait for it
+    without blocking (a dependency may sit in another lane of the warp)."""
+    rng = np.random.default_rng(100 + k)
+    Ms = leveled_lower([5000] * 4, k, rng, window=4000)  # strictly lower: the unit kinds
+    b = rng.standard_normal(Ms.ncols)
+    for kind in (L.TRI_LOWER_UNIT, L.TRI_LOWER_T_UNIT):
+        check(Ms, kind, b, monkeypatch)
+    n = Ms.ncols
+    cols = np.repeat(np.arange(n), np.diff(Ms.col_ptr))
+    M = P.CscMatrix.from_coo(n, n, np.concatenate([Ms.row_idx, np.arange(n)]), np.concatenate([cols, np.arange(n)]),
+                             np.concatenate([Ms.values, rng.uniform(1.0, 2.0, n)]))
+    for kind in (L.TRI_LOWER, L.TRI_LOWER_T):
+        check(M, kind, b, monkeypatch)
+    U = transpose(M)
+    for kind in (L.TRI_UPPER, L.TRI_UPPER_T):
+        check(U, kind, b, monkeypatch)
+    assert variant(M, L.TRI_LOWER)[0] == "grid"
+
+
 def test_many_chunks_every_kind(monkeypatch):
     rng = np.random.default_rng(3)
     M = leveled_lower([64] * 700, 8, rng, diag=lambda n: rng.uniform(1.0, 2.0, n) * rng.choice([-1, 1], n))
