@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(kWideBlock) k_trsv_wide(TriDev T, const double
         T.prof[7] = (long long)ts;
     }
     while (s < nslices) {
-        const int s_next = take();  // latency overlaps this slice
+        // (no early ticket: a slice held while the warp works on another is
+        // never ready-and-loaded when its level is reached)
         const int t = s * 32 + lane;
         const bool valid = t < T.n;
         const int64_t base = T.slice_off[s];
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kWideBlock) k_trsv_wide(TriDev T, const double
             }
             __syncwarp();
         }
-        s = s_next;
+        s = take();
     }
 }
 
