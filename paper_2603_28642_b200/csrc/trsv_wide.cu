@@ -84,7 +84,7 @@ __device__ __noinline__ double wide_tail(const TriDev &T, int64_t base, int lane
 }
 
 template <int MODE, int N>
-__global__ void __launch_bounds__(kWideBlock) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
+__global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
                                                           Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
