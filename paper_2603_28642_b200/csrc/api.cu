@@ -133,6 +133,8 @@ int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
     ctx->device = device;
     ctx->flags = flags;
     cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    for (int i = 0; e == cudaSuccess && i < 3; ++i) e = cudaEventCreateWithFlags(&ctx->fork_ev[i], cudaEventDisableTiming);
     for (int i = 0; e == cudaSuccess && i < 16; ++i) e = cudaEventCreate(&ctx->ev[i]);
     for (int i = 0; e == cudaSuccess && i < 64; ++i) e = cudaEventCreate(&ctx->trace_ev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&ctx->h_scalar, 64 * sizeof(double));
@@ -167,6 +169,9 @@ int rsb_ctx_destroy(rsb_ctx *ctx) {
     for (auto &e : ctx->trace_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->flush_buf) dev_free(ctx, ctx->flush_buf, ctx->flush_bytes);
+    for (auto &e : ctx->fork_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return RSB_OK;

@@ -240,6 +240,10 @@ struct rsb_ctx {
     int device = 0;
     int flags = 0;
     cudaStream_t stream = nullptr;
+    // a second stream for graph branches off the critical path (the pcgls
+    // iteration's ||x|| and z.z dots), with the events that fork and join it
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev[3] = {};
     int64_t launches = 0;
     int64_t mem_bytes = 0;
     cudaEvent_t ev[16] = {};
