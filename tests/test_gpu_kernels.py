@@ -170,7 +170,8 @@ def test_power_method_matches_oracle():
         P.power_method_norm2(A, 0)
 
 
-@pytest.mark.parametrize("n", [1, 15, 16, 17, 31, 32, 33, 48, 100, 1000, 65536, 98304, 1_000_003])
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 31, 32, 33, 48, 100, 1000, 12287, 12288, 12303, 12320, 32 * 256 + 31,
+                               32 * (1024 * 3 + 16 * 5 + 7) + 20, 65536, 98304, 1_000_003, 1_500_000])
 def test_device_dot_reference_order(n):
     from paper_2603_28642_b200 import _lib as L
     from paper_2603_28642_b200.device import get_context
