@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--batch", type=int, default=8,
                     help="also time this many concurrent RHS per GPU through pcgls_batch (0: skip)")
+    ap.add_argument("--blas-threads", type=int, default=1,
+                    help="reproduce the reference's OpenBLAS dot order at this many threads "
+                         "(OPENBLAS_NUM_THREADS; 1 = the pinned single-thread order)")
     ap.add_argument("--partition", default="replicas", choices=["replicas", "rows"],
                     help="N>1: replicas (one RHS per GPU, weak) or rows (one RHS, A row-partitioned, "
                          "NCCL allreduce of A^T r, strong)")
@@ -234,6 +237,7 @@ def cpu_oracle_rate(S, pre, b, norm_a, budget_s, max_iters_cap=400):
     from oracle import oracle as O
 
     op = O.OraclePreconditioner.from_reference(pre)
+    O.set_blas_threads(int(os.environ.get("RSB_BLAS_THREADS", "1")))
     t0 = time.perf_counter()
     O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=2)
     probe = max(time.perf_counter() - t0, 1e-4) / 2
@@ -250,6 +254,8 @@ def run_reference(args):
         return
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import oracle as O
+
+    O.set_blas_threads(args.blas_threads)
 
     A, b, st, name, _ = make_workload(args, 0)
     S, f, pre, mode, _ = setup(args, A, st)
@@ -419,7 +425,8 @@ def run_b200(args):
             "l2": "flushed (320 MiB write) before every timed iteration, outside the event bracket"
                   if not args.no_flush else "not flushed",
             "parallelism": f"replicas x{world} (one RHS per GPU)",
-            "dot_order": "exact (reference OpenBLAS association)",
+            "dot_order": (f"exact (reference OpenBLAS association, {args.blas_threads} thread"
+                          f"{'s' if args.blas_threads > 1 else ''})"),
         },
         "roofline": {
             "kernel": "triangular solves (+ k_gather_pos), 8 per cg(2) iteration: "
@@ -494,6 +501,7 @@ def run_rows(args):
 
 def main():
     args = parse()
+    os.environ["RSB_BLAS_THREADS"] = str(args.blas_threads)
     if args.impl == "reference":
         run_reference(args)
     elif args.partition == "rows" and int(os.environ.get("WORLD_SIZE", "1")) > 1:

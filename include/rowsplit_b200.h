@@ -48,6 +48,11 @@ extern "C" {
 /* context flags: reduction order for dots and norms */
 #define RSB_DOT_EXACT 0 /* reference (OpenBLAS ddot) association: bitwise parity */
 #define RSB_DOT_TREE 1  /* fixed-order two-level tree: deterministic, faster for n >> 1e6 */
+/* exact order of the reference's OpenBLAS running T threads (OPENBLAS_NUM_THREADS=T
+ * on a host with >= T cores, T <= 64): a dot longer than 10000 is split into T
+ * contiguous chunks of widths ceil(rest / threads left), each reduced in the
+ * one-thread order, partials summed in chunk order.  T = 0 or 1: one thread. */
+#define RSB_DOT_BLAS_THREADS(t) (((t) & 0xFF) << 8)
 
 /* triangular solve kinds (sc.py:243-313) */
 #define RSB_TRI_LOWER 0        /* sparse_lower_solve(L, b, unit_diag=False)  sc.py:243 */

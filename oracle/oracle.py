@@ -167,14 +167,49 @@ def dense_cholesky_solve(g, b):
     return x
 
 
+_blas_threads = int(os.environ.get("RSB_BLAS_THREADS", "1") or 1)
+
+
+def set_blas_threads(t: int) -> int:
+    """OpenBLAS thread count T the reference ran with (OPENBLAS_NUM_THREADS=T
+    on a host with >= T cores); returns the previous value."""
+    global _blas_threads
+    if not 1 <= int(t) <= 64:
+        raise ValueError("blas threads must be in 1..64")
+    prev, _blas_threads = _blas_threads, int(t)
+    return prev
+
+
+def blas_chunks(n: int, t: int) -> list[int]:
+    """OpenBLAS's split of an n-long ddot over t threads
+    (driver/others/blas_l1_thread.c): n <= 10000 runs on one thread,
+    otherwise widths ceil(rest / threads left)."""
+    if t <= 1 or n <= 10000:
+        return [n]
+    out, rest = [], n
+    for i in range(t):
+        w = -(-rest // (t - i))
+        out.append(w)
+        rest -= w
+    return out
+
+
 def dot(a, b):
     """`a @ b` for 1-D float64 as the reference host's OpenBLAS computes it
-    (single thread; rsref.c rso_blas_dot)."""
+    (rsref.c rso_blas_dot per thread; with T threads the chunk results are
+    summed in thread order from 0.0, interface/dot.c)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     if a.shape != b.shape:
         raise ValueError("dot: shape mismatch")
-    return lib().rso_blas_dot(len(a), _pf(a), _pf(b))
+    widths = blas_chunks(len(a), _blas_threads)
+    if len(widths) == 1:
+        return lib().rso_blas_dot(len(a), _pf(a), _pf(b))
+    total, lo = 0.0, 0
+    for w in widths:
+        total = total + lib().rso_blas_dot(w, _pf(a[lo:lo + w]), _pf(b[lo:lo + w]))
+        lo += w
+    return total
 
 
 def norm(a):

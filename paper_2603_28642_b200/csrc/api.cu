@@ -149,6 +149,13 @@ int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
         ctx->partial_cap = 2 * 148 * 4;
         rc = dev_alloc(ctx, (void **)&ctx->d_partials, ctx->partial_cap * sizeof(double));
     }
+    ctx->blas_threads = std::max(1, std::min(kMaxBlasThreads, (flags >> 8) & 0xFF));
+    if (rc == RSB_OK) rc = dev_alloc(ctx, (void **)&ctx->d_dot_part, (size_t)kDotSlots * kMaxBlasThreads * sizeof(double));
+    if (rc == RSB_OK) rc = dev_alloc(ctx, (void **)&ctx->d_dot_cnt, kDotSlots * sizeof(unsigned));
+    if (rc == RSB_OK && cudaMemset(ctx->d_dot_cnt, 0, kDotSlots * sizeof(unsigned)) != cudaSuccess) {
+        set_error("context setup failed: memset");
+        rc = RSB_ECUDA;
+    }
     if (rc != RSB_OK) {
         delete ctx;
         return rc;
@@ -163,6 +170,8 @@ int rsb_ctx_destroy(rsb_ctx *ctx) {
     cudaStreamSynchronize(ctx->stream);
     dev_free(ctx, ctx->d_scalar, 64 * sizeof(double));
     dev_free(ctx, ctx->d_partials, ctx->partial_cap * sizeof(double));
+    dev_free(ctx, ctx->d_dot_part, (size_t)kDotSlots * kMaxBlasThreads * sizeof(double));
+    dev_free(ctx, ctx->d_dot_cnt, kDotSlots * sizeof(unsigned));
     if (ctx->h_scalar) cudaFreeHost(ctx->h_scalar);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);

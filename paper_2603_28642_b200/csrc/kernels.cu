@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "device_common.cuh"
 #include "rsb_internal.h"
@@ -91,12 +93,49 @@ __device__ __forceinline__ double warp_blas_dot(int64_t n, LA la, LB lb) {
     return warp_blas_finish(acc, n, la, lb);
 }
 
+// OpenBLAS with T threads (interface ddot, n > 10000): T contiguous chunks of
+// widths ceil(rem / threads left), each reduced by the one-thread kernel
+// above, the partial results summed in chunk order from 0.0
+// (blas_level1_thread_with_return_value; verified bit for bit against numpy
+// at OPENBLAS_NUM_THREADS = 2, 3, 4, 8 by tests/test_oracle_pin.py).
+// Block t of the launch reduces chunk t.
+__device__ __forceinline__ void dot_chunk(int64_t n, int T, int t, int64_t &lo, int64_t &w) {
+    lo = 0;
+    int64_t rem = n;
+    for (int i = 0; i < t; ++i) {
+        const int64_t wi = (rem + (T - i) - 1) / (T - i);
+        lo += wi;
+        rem -= wi;
+    }
+    w = (rem + (T - t) - 1) / (T - t);
+}
+
+// lane 0 of every block: publish this chunk's result; the last block to
+// finish sums the partials in chunk order and writes the dot
+__device__ __forceinline__ void dot_combine(double d, double *out, int sqrt_out, const DotChunks &c) {
+    if (c.T <= 1) {
+        out[0] = sqrt_out ? sqrt(d) : d;
+        return;
+    }
+    c.part[blockIdx.x] = d;
+    __threadfence();
+    const unsigned prev = atomicAdd(c.cnt, 1u);
+    if (prev != (unsigned)c.T - 1) return;
+    __threadfence();
+    double sum = 0.0;
+    for (int i = 0; i < c.T; ++i) sum = __dadd_rn(sum, ((volatile const double *)c.part)[i]);
+    out[0] = sqrt_out ? sqrt(sum) : sum;
+    *c.cnt = 0;  // ready for the next replay of the graph
+}
+
 __global__ void k_dot_exact(int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
-                            const int *need) {
+                            const int *need, DotChunks ch) {
     if (gated(g) || (need && !*(volatile const int *)need)) return;
+    int64_t lo = 0, w = n;
+    if (ch.T > 1) dot_chunk(n, ch.T, blockIdx.x, lo, w);
     double d = warp_blas_dot(
-        n, [&](int64_t i) { return vin(a, i); }, [&](int64_t i) { return vin(b, i); });
-    if (threadIdx.x == 0) out[0] = sqrt_out ? sqrt(d) : d;
+        w, [&](int64_t i) { return vin(a, lo + i); }, [&](int64_t i) { return vin(b, lo + i); });
+    if (threadIdx.x == 0) dot_combine(d, out, sqrt_out, ch);
 }
 
 // Fixed-shape two-level tree (RSB_DOT_TREE): block b sums a fixed chunk in a
@@ -148,35 +187,155 @@ __global__ void __launch_bounds__(kBlock) k_spmv(Compressed A, VecIn x, double *
     y[i] = acc;
 }
 
-// numpy pairwise summation (DOUBLE_pairwise_sum) of products val[k]*y[idx[k]],
-// k = lo .. lo+n-1
-__device__ double pw_prod(const double *val, const int32_t *idx, const VecIn &y, int64_t lo,
-                          int64_t n) {
+// numpy pairwise summation (DOUBLE_pairwise_sum): below 8 terms sequential
+// from -0.0; up to 128 eight strided accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail; above, split at
+// n/2 rounded down to a multiple of 8.  term(k) yields the k-th term.
+template <class Term>
+__device__ __forceinline__ double pw_leaf(const Term &term, int64_t o, int64_t n) {
     if (n < 8) {
         double r = -0.0;
-        for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, __dmul_rn(val[lo + i], vin(y, idx[lo + i])));
+        for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, term(o + i));
         return r;
     }
-    if (n <= 128) {
-        double r[8];
+    double r[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) r[k] = __dmul_rn(val[lo + k], vin(y, idx[lo + k]));
-        int64_t i = 8;
-        for (; i < n - (n % 8); i += 8) {
+    for (int k = 0; k < 8; ++k) r[k] = term(o + k);
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                r[k] = __dadd_rn(r[k], __dmul_rn(val[lo + i + k], vin(y, idx[lo + i + k])));
-        }
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn(val[lo + i], vin(y, idx[lo + i])));
-        return res;
+        for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], term(o + i + k));
     }
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    double left = pw_prod(val, idx, y, lo, n2);
-    double right = pw_prod(val, idx, y, lo + n2, n - n2);
-    return __dadd_rn(left, right);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, term(o + i));
+    return res;
+}
+
+// The split levels as a chain of distinct non-inlined functions (depth D
+// covers n < 128 * 2^D), so the stack is sized statically: no device
+// recursion.
+template <int D, class Term>
+struct Pairwise {
+    static __device__ __noinline__ double sum(const Term &term, int64_t o, int64_t n) {
+        if (n <= 128) return pw_leaf(term, o, n);
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        const double left = Pairwise<D - 1, Term>::sum(term, o, n2);
+        return __dadd_rn(left, Pairwise<D - 1, Term>::sum(term, o + n2, n - n2));
+    }
+};
+template <class Term>
+struct Pairwise<0, Term> {
+    static __device__ __noinline__ double sum(const Term &term, int64_t o, int64_t n) { return pw_leaf(term, o, n); }
+};
+
+// products val[k]*y[idx[k]], k = lo .. lo+n-1 (n < 2^31)
+__device__ __forceinline__ double pw_prod(const double *val, const int32_t *idx, const VecIn &y, int64_t lo,
+                                          int64_t n) {
+    struct Term {
+        const double *val;
+        const int32_t *idx;
+        const VecIn *y;
+        __device__ double operator()(int64_t k) const { return __dmul_rn(val[k], vin(*y, idx[k])); }
+    };
+    const Term t{val + lo, idx + lo, &y};
+    if (n <= 128) return pw_leaf(t, 0, n);
+    return Pairwise<25, Term>::sum(t, 0, n);
+}
+
+// already formed products p[0 .. n-1] (shared memory; n <= kSpCap < 128 * 2^5)
+__device__ __forceinline__ double pw_smem(const double *p, int n) {
+    struct Term {
+        const double *p;
+        __device__ double operator()(int64_t k) const { return p[k]; }
+    };
+    const Term t{p};
+    if (n <= 128) return pw_leaf(t, 0, n);
+    return Pairwise<5, Term>::sum(t, 0, n);
+}
+
+// ---------------------------------------------------------------------------
+// Tiled SpMV (default).  A block owns kBlock consecutive lines (rows of the
+// CSR / columns of the CSC).  Phase 1 streams the tile's entries with
+// coalesced loads -- consecutive threads take consecutive entries, four in
+// flight per thread -- and forms every product val * x[idx] (the products
+// are independent: only the summation order is fixed), into shared memory.
+// Phase 2: thread t sums line t's products in the reference's order
+// (sequential from 0.0 for A x; p0 + pairwise for A^T y).  A tile whose
+// entries exceed the staging buffer (a long line: config 2's dense rows)
+// runs the thread-per-line loop instead, with the same order.
+// ---------------------------------------------------------------------------
+constexpr int kSpCap = 3072;  // staged products per tile (24 KB): 12 per line
+
+__device__ __forceinline__ void stage_products(const Compressed &A, const VecIn &x, int lo, int hi,
+                                               double *prod) {
+    int k = lo + threadIdx.x;
+    for (; k + 3 * kBlock < hi; k += 4 * kBlock) {
+        int c[4];
+        double v[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            c[u] = __ldcs(A.idx + k + u * kBlock);
+            v[u] = __ldcs(A.val + k + u * kBlock);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = vin(x, c[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) prod[k + u * kBlock - lo] = __dmul_rn(v[u], xv[u]);
+    }
+    for (; k < hi; k += kBlock) prod[k - lo] = __dmul_rn(__ldcs(A.val + k), vin(x, __ldcs(A.idx + k)));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) k_spmv_tile(Compressed A, VecIn x, double *y, VecIn e, Gate g) {
+    if (gated(g)) return;
+    __shared__ double prod[kSpCap];
+    const int64_t l0 = blockIdx.x * (int64_t)kBlock;
+    const int64_t i = l0 + threadIdx.x;
+    const bool valid = i < A.nlines;
+    const int64_t lend = min((int64_t)A.nlines, l0 + kBlock);
+    const int lo = A.ptr[l0], hi = A.ptr[lend];
+    double acc = 0.0;
+    if (hi - lo <= kSpCap) {
+        stage_products(A, x, lo, hi, prod);
+        __syncthreads();
+        if (!valid) return;
+        const int s = A.ptr[i] - lo, t = A.ptr[i + 1] - lo;
+        for (int k = s; k < t; ++k) acc = __dadd_rn(acc, prod[k]);
+    } else {
+        if (!valid) return;
+        const int s = A.ptr[i], t = A.ptr[i + 1];
+        for (int k = s; k < t; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], vin(x, A.idx[k])));
+    }
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, i), acc);
+    if (EPI == EPI_SUB_FROM) acc = __dsub_rn(vin(e, i), acc);
+    y[i] = acc;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlock, 4) k_spmv_t_tile(Compressed At, VecIn y, double *z, VecIn e, Gate g) {
+    if (gated(g)) return;
+    __shared__ double prod[kSpCap];
+    const int64_t l0 = blockIdx.x * (int64_t)kBlock;
+    const int64_t j = l0 + threadIdx.x;
+    const bool valid = j < At.nlines;
+    const int64_t lend = min((int64_t)At.nlines, l0 + kBlock);
+    const int lo = At.ptr[l0], hi = At.ptr[lend];
+    double acc = 0.0;
+    if (hi - lo <= kSpCap) {
+        stage_products(At, y, lo, hi, prod);
+        __syncthreads();
+        if (!valid) return;
+        const int s = At.ptr[j] - lo, t = At.ptr[j + 1] - lo;
+        if (t > s) acc = __dadd_rn(prod[s], pw_smem(prod + s + 1, t - s - 1));
+    } else {
+        if (!valid) return;
+        const int s = At.ptr[j], t = At.ptr[j + 1];
+        if (t > s) acc = __dadd_rn(__dmul_rn(At.val[s], vin(y, At.idx[s])), pw_prod(At.val, At.idx, y, s + 1, t - s - 1));
+    }
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, j), acc);
+    z[j] = acc;
 }
 
 // z = A^T y: np.add.reduceat over the column's products (sc.py:231-234)
@@ -440,12 +599,23 @@ __device__ __forceinline__ double canonical(double v) {
 // association as k_dot_exact, with both operands streamed through shared
 // memory by TMA bulk copies (kDotStages-deep mbarrier pipeline) so the FMA
 // chain waits on shared-memory, not global-memory, latency.
-__global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double *a, const double *b, double *out,
-                                                         int sqrt_out, Gate g, const int *need) {
+__global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const double *a_all, const double *b_all,
+                                                         double *out, int sqrt_out, Gate g, const int *need,
+                                                         DotChunks ch) {
     if (gated(g) || (need && !*(volatile const int *)need)) return;
     extern __shared__ __align__(16) double dbuf[];
-    unsigned long long *bar = reinterpret_cast<unsigned long long *>(dbuf + kDotStages * 2 * kDotChunk);
+    constexpr int kBuf = kDotChunk + 2;  // one stage of one operand: a chunk shifted by <= 1 element
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(dbuf + kDotStages * 2 * kBuf);
     const int lane = threadIdx.x;
+    // this block's chunk [lo, lo + n) of the operands (the whole vector when T = 1)
+    int64_t lo = 0, n = n_all;
+    if (ch.T > 1) dot_chunk(n_all, ch.T, blockIdx.x, lo, n);
+    const double *a = a_all + lo, *b = b_all + lo;
+    // bulk copies need 16-byte aligned sources and sizes: copy from the even
+    // element below each stage's start (shift = lo & 1 elements into the
+    // buffer) to the even element above its end, except past the end of the
+    // vectors, where the last odd element is loaded by lane 0 instead
+    const int shift = (int)(lo & 1);
     const int64_t n32 = (n & ~(int64_t)15) & ~(int64_t)31;
     const int64_t nch = (n32 + kDotChunk - 1) / kDotChunk;
     if (lane == 0) {
@@ -453,13 +623,25 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
+    auto span = [&](int64_t c, int64_t &c0, int64_t &c1, bool &patch) {
+        const int64_t e0 = lo + c * kDotChunk, e1 = lo + min((int64_t)kDotChunk * (c + 1), n32);
+        c0 = e0 & ~(int64_t)1;
+        c1 = (e1 + 1) & ~(int64_t)1;
+        patch = c1 > n_all;
+        if (patch) c1 -= 2;
+    };
     auto issue = [&](int64_t c) {
         const int st = (int)(c % kDotStages);
-        const int64_t e0 = c * kDotChunk, cnt = min((int64_t)kDotChunk, n32 - e0);
+        int64_t c0, c1;
+        bool patch;
+        span(c, c0, c1, patch);
+        const unsigned bytes = (unsigned)((c1 - c0) * 8);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[st], (unsigned)(2 * cnt * 8));
-        bulk_g2s(dbuf + (size_t)st * 2 * kDotChunk, a + e0, (unsigned)(cnt * 8), &bar[st]);
-        bulk_g2s(dbuf + (size_t)st * 2 * kDotChunk + kDotChunk, b + e0, (unsigned)(cnt * 8), &bar[st]);
+        mbar_expect_tx(&bar[st], 2 * bytes);
+        if (bytes) {
+            bulk_g2s(dbuf + (size_t)st * 2 * kBuf, a_all + c0, bytes, &bar[st]);
+            bulk_g2s(dbuf + (size_t)st * 2 * kBuf + kBuf, b_all + c0, bytes, &bar[st]);
+        }
     };
     if (lane == 0)
         for (int64_t c = 0; c < min((int64_t)kDotStages, nch); ++c) issue(c);
@@ -467,7 +649,18 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double
     for (int64_t c = 0; c < nch; ++c) {
         const int st = (int)(c % kDotStages);
         mbar_wait_spin(&bar[st], (unsigned)((c / kDotStages) & 1));
-        const double *sa = dbuf + (size_t)st * 2 * kDotChunk + lane, *sb = sa + kDotChunk;
+        double *buf_a = dbuf + (size_t)st * 2 * kBuf, *buf_b = buf_a + kBuf;
+        {
+            int64_t c0, c1;
+            bool patch;
+            span(c, c0, c1, patch);
+            if (patch && lane == 0) {  // the vectors' last element (odd index) was not copied
+                buf_a[c1 - c0] = a_all[c1];
+                buf_b[c1 - c0] = b_all[c1];
+            }
+            __syncwarp();
+        }
+        const double *sa = buf_a + shift + lane, *sb = buf_b + shift + lane;
         const int steps = (int)min((int64_t)kDotChunk, n32 - c * kDotChunk) / 32;
         // the lane's FMA chain, 8 cycles a step: operands of the next 8 steps
         // are loaded while the current 8 issue, so the chain never waits on
@@ -503,7 +696,7 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n, const double
         if (lane == 0 && c + kDotStages < nch) issue(c + kDotStages);
     }
     const double d = warp_blas_finish(acc, n, [&](int64_t i) { return a[i]; }, [&](int64_t i) { return b[i]; });
-    if (lane == 0) out[0] = sqrt_out ? sqrt(d) : d;
+    if (lane == 0) dot_combine(d, out, sqrt_out, ch);
 }
 
 // right-hand side in task-position order: bpos[t] = a(row_t) [+ c[row_t]]
@@ -866,9 +1059,26 @@ inline int post_launch(rsb_ctx *ctx, int kernels = 1) {
 
 }  // namespace
 
+// RSB_SPMV=thread selects the thread-per-line kernels (experiments)
+static bool spmv_tiled() {
+    static const int tiled = [] {
+        const char *v = getenv("RSB_SPMV");
+        return (v && strcmp(v, "thread") == 0) ? 0 : 1;
+    }();
+    return tiled != 0;
+}
+
 int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
     if (A.nlines == 0) return RSB_OK;
     const int grid = grid_for(A.nlines, kBlock);
+    if (spmv_tiled()) {
+        switch (epi) {
+            case EPI_STORE: k_spmv_tile<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+            case EPI_ADD: k_spmv_tile<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+            default: k_spmv_tile<EPI_SUB_FROM><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+        }
+        return post_launch(ctx);
+    }
     switch (epi) {
         case EPI_STORE: k_spmv<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
         case EPI_ADD: k_spmv<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
@@ -880,6 +1090,13 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
 int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
     if (At.nlines == 0) return RSB_OK;
     const int grid = grid_for(At.nlines, kBlock);
+    if (spmv_tiled()) {
+        if (epi == EPI_ADD)
+            k_spmv_t_tile<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        else
+            k_spmv_t_tile<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        return post_launch(ctx);
+    }
     if (epi == EPI_ADD)
         k_spmv_t<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
     else
@@ -1023,18 +1240,25 @@ int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_
         k_dot_tree_final<<<1, 32, 0, ctx->stream>>>(parts, ctx->d_partials, out, sqrt_out, g, need);
         return post_launch(ctx);
     }
+    // the reference's OpenBLAS runs dots longer than 10000 on T threads
+    DotChunks ch{1, nullptr, nullptr};
+    if (ctx->blas_threads > 1 && n > 10000) {
+        const int slot = ctx->dot_slot++ % kDotSlots;
+        ch = DotChunks{ctx->blas_threads, ctx->d_dot_part + (size_t)slot * kMaxBlasThreads, ctx->d_dot_cnt + slot};
+    }
+    const int64_t per_chunk = n / ch.T;
     const bool plain = !a.g && !b.g && !a.off && !b.off && ((uintptr_t)a.p % 16 == 0) && ((uintptr_t)b.p % 16 == 0);
-    if (plain && n >= 2 * kDotChunk) {
-        const size_t smem = (size_t)kDotStages * 2 * kDotChunk * 8 + kDotStages * 8;
-        k_dot_exact_staged<<<1, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need);
+    if (plain && per_chunk >= 2 * kDotChunk) {
+        const size_t smem = (size_t)kDotStages * 2 * (kDotChunk + 2) * 8 + kDotStages * 8;
+        k_dot_exact_staged<<<ch.T, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need, ch);
         return post_launch(ctx);
     }
-    k_dot_exact<<<1, 32, 0, ctx->stream>>>(n, a, b, out, sqrt_out, g, need);
+    k_dot_exact<<<ch.T, 32, 0, ctx->stream>>>(n, a, b, out, sqrt_out, g, need, ch);
     return post_launch(ctx);
 }
 
 int prepare_kernels() {
-    const int smem = kDotStages * 2 * kDotChunk * 8 + kDotStages * 8;
+    const int smem = kDotStages * 2 * (kDotChunk + 2) * 8 + kDotStages * 8;
     RSB_TRY_CUDA(cudaFuncSetAttribute(k_dot_exact_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return RSB_OK;
 }

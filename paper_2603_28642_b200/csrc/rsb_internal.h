@@ -236,9 +236,23 @@ struct TriSched {
 
 }  // namespace rsb
 
+// OpenBLAS-thread emulation of the exact dot order (RSB_DOT_BLAS_THREADS):
+// per launch, T chunk partials and a completion counter in a ring of slots
+constexpr int kMaxBlasThreads = 64;  // OpenBLAS MAX_THREADS of the reference's numpy wheel
+constexpr int kDotSlots = 256;
+struct DotChunks {
+    int T;            // chunks (1: the one-thread order, no combine)
+    double *part;     // T partial results
+    unsigned *cnt;    // blocks done (the last one combines and resets it)
+};
+
 struct rsb_ctx {
     int device = 0;
     int flags = 0;
+    int blas_threads = 1;  // OpenBLAS threads the exact dot order reproduces
+    double *d_dot_part = nullptr;
+    unsigned *d_dot_cnt = nullptr;
+    int64_t dot_slot = 0;
     cudaStream_t stream = nullptr;
     // a second stream for graph branches off the critical path (the pcgls
     // iteration's ||x|| and z.z dots), with the events that fork and join it

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib as L
 
 _ctx_lock = threading.Lock()
-_contexts: dict[int, "Context"] = {}
+_contexts: dict[tuple, "Context"] = {}
 _exiting = False
 
 
@@ -48,8 +48,22 @@ def default_device() -> int:
     return int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def blas_threads() -> int:
+    """OpenBLAS thread count whose ddot association the exact dot order
+    reproduces (RSB_BLAS_THREADS, default 1: the reference run with
+    OPENBLAS_NUM_THREADS=1).  The reference's numpy splits a dot longer than
+    10000 over min(OPENBLAS_NUM_THREADS, cores) threads, at most 64."""
+    t = int(os.environ.get("RSB_BLAS_THREADS", "1") or 1)
+    if not 1 <= t <= 64:
+        raise ValueError("RSB_BLAS_THREADS must be in 1..64")
+    return t
+
+
 def dot_flags() -> int:
-    return L.RSB_DOT_TREE if os.environ.get("RSB_DOT_ORDER", "exact") == "tree" else L.RSB_DOT_EXACT
+    if os.environ.get("RSB_DOT_ORDER", "exact") == "tree":
+        return L.RSB_DOT_TREE
+    t = blas_threads()
+    return L.RSB_DOT_EXACT | ((t << 8) if t > 1 else 0)
 
 
 class Context:
@@ -94,11 +108,12 @@ class Context:
 
 def get_context(device: int | None = None) -> Context:
     dev = default_device() if device is None else device
+    flags = dot_flags()
     with _ctx_lock:
-        ctx = _contexts.get(dev)
+        ctx = _contexts.get((dev, flags))
         if ctx is None:
-            ctx = Context(dev)
-            _contexts[dev] = ctx
+            ctx = Context(dev, flags)
+            _contexts[(dev, flags)] = ctx
         return ctx
 
 
@@ -200,7 +215,7 @@ _mat_cache: "collections.OrderedDict[tuple, tuple]" = collections.OrderedDict()
 
 def device_matrix(A, ctx: Context | None = None) -> DeviceMatrix:
     ctx = ctx or get_context()
-    key = (id(A), ctx.device)
+    key = (id(A), id(ctx))
     hit = _mat_cache.get(key)
     if hit is not None and hit[0] is A:
         _mat_cache.move_to_end(key)
@@ -294,7 +309,7 @@ _pre_cache: "collections.OrderedDict[tuple, tuple]" = collections.OrderedDict()
 
 def device_preconditioner(pre, ctx: Context | None = None) -> DevicePreconditioner:
     ctx = ctx or get_context()
-    key = (id(pre), ctx.device)
+    key = (id(pre), id(ctx))
     hit = _pre_cache.get(key)
     if hit is not None and hit[0] is pre:
         _pre_cache.move_to_end(key)
@@ -365,19 +380,20 @@ def device_solver(dA: DeviceMatrix, dpre: DevicePreconditioner | None) -> Device
     return s
 
 
-_stream_pool: dict[int, list[Context]] = {}
+_stream_pool: dict[tuple, list[Context]] = {}
 
 
 def stream_contexts(k: int, device: int | None = None) -> list[Context]:
     """k distinct contexts (streams) on one device for concurrent solves; the
     first is the device's default context."""
     dev = default_device() if device is None else device
+    flags = dot_flags()
     with _ctx_lock:
-        pool = _stream_pool.setdefault(dev, [])
+        pool = _stream_pool.setdefault((dev, flags), [])
     first = get_context(dev)
     with _ctx_lock:
         while len(pool) < k - 1:
-            pool.append(Context(dev))
+            pool.append(Context(dev, flags))
         return [first] + pool[: k - 1]
 
 

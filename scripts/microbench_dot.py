@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_28642_b200 import _lib as L
 from paper_2603_28642_b200.device import DeviceBuffer, get_context
 ctx = get_context(); out = {}
-for n in (32768, 65536, 98304, 1 << 20):
+for n in (32768, 65536, 98304, 1 << 20, 8_000_000, 16_000_000):
     rng = np.random.default_rng(n); a = DeviceBuffer(ctx, n); b = DeviceBuffer(ctx, n)
     a.upload(rng.standard_normal(n)); b.upload(rng.standard_normal(n)); r = np.zeros(1); ts = []
     for k in range(13):

@@ -70,14 +70,13 @@ def test_oracle_pairwise_reduceat(K):
         assert got == want
 
 
-@pytest.mark.parametrize("name", ["cfg0s_mu0.1", "cfg0s_mu1.0", "cfg1s_mu1.0"])
-def test_oracle_apply_and_pcgls_bitwise(name):
+def _oracle_matches_fixture(name, pm_seed):
     z = golden(f"{name}.npz")
     meta = golden_json(f"{name}_reports.json")
     S = csc_from(z, "S")
     f = factors_from(z)
     b, norm_a = z["b"], float(z["norm_a"])
-    assert O.power_method_norm2(S, 100, 0) == norm_a
+    assert O.power_method_norm2(S, 100, pm_seed) == norm_a
     for mode, want in meta["reports"].items():
         if mode == "plain":
             x, rep = O.pcgls(S, b, None, norm_a, delta=meta["delta"], max_iters=meta["max_iters"])
@@ -93,6 +92,45 @@ def test_oracle_apply_and_pcgls_bitwise(name):
             x, rep = O.pcgls(S, b, pre, norm_a, delta=meta["delta"], max_iters=meta["max_iters"])
         assert np.array_equal(x, z[f"x_{mode}"]), mode
         assert rep == want, mode
+
+
+@pytest.mark.parametrize("name", ["cfg0s_mu0.1", "cfg0s_mu1.0", "cfg1s_mu1.0"])
+def test_oracle_apply_and_pcgls_bitwise(name):
+    _oracle_matches_fixture(name, 0)
+
+
+@pytest.fixture
+def blas_threads():
+    prev = O.set_blas_threads(1)
+    yield O.set_blas_threads
+    O.set_blas_threads(prev)
+
+
+def test_oracle_blas_threads_split():
+    """OpenBLAS's thread split (blas_l1_thread.c): one thread up to 10000."""
+    assert O.blas_chunks(10000, 8) == [10000]
+    assert O.blas_chunks(10001, 8) == [1251, 1250, 1250, 1250, 1250, 1250, 1250, 1250]
+    assert O.blas_chunks(20001, 3) == [6667, 6667, 6667]
+    assert sum(O.blas_chunks(1000003, 64)) == 1000003
+
+
+def test_oracle_blas_threads_dot_order(blas_threads):
+    """The reference's numpy at OPENBLAS_NUM_THREADS = 2, 4, 8 (dots_mt.json,
+    tests/golden/make_golden_mt.py)."""
+    g = golden_json("dots_mt.json")
+    for t, vals in g["dots"].items():
+        blas_threads(int(t))
+        rng = np.random.default_rng(g["seed"])
+        for n, want in zip(g["lens"], vals):
+            a, b = rng.standard_normal(n), rng.standard_normal(n)
+            assert O.dot(a, b) == want, (t, n)
+
+
+def test_oracle_pcgls_blas_threads_golden(blas_threads):
+    """The whole reference pipeline run with OPENBLAS_NUM_THREADS=8 on a
+    112^2-grid config 1 (every n- and m-long dot and norm threaded)."""
+    blas_threads(8)
+    _oracle_matches_fixture("cfg1m_t8", 1)
 
 
 def test_oracle_identity_golden():
