@@ -121,12 +121,14 @@ int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
 /* which kernel runs the (matrix, kind) solve: RSB_TRSV_GRID (sync-free
  * grid-wide, wide DAGs), RSB_TRSV_STAGED (one CTA, staged records),
  * RSB_TRSV_LEAN (one CTA, register-pipelined; *lean_n = its longest task,
- * else 0) or RSB_TRSV_LEVELS (a grid launch per level: wide DAGs with few
- * levels) */
+ * else 0), RSB_TRSV_LEVELS (a grid launch per level: wide DAGs with few
+ * levels) or RSB_TRSV_LSYNC (one persistent launch, items of one level
+ * taken in level order, a level waits on the previous one's completion) */
 #define RSB_TRSV_GRID 0
 #define RSB_TRSV_STAGED 1
 #define RSB_TRSV_LEAN 2
 #define RSB_TRSV_LEVELS 3
+#define RSB_TRSV_LSYNC 4 /* persistent level-synchronous grid solve (wide, shallow DAGs; default there) */
 int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n);
 /* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),
  * drawn by the caller (host RNG stays on the host). */

@@ -426,6 +426,24 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         if (gv && std::strcmp(gv, "levels") == 0) S->level_launch = true;
         if (gv && std::strcmp(gv, "syncfree") == 0) S->level_launch = false;
         S->h_level_ptr = lptr;
+        // level-synchronous items (trsv_lsync.cu): the default for wide DAGs of
+        // at most kLsMaxLevels levels
+        S->lsync = S->wide && nlev <= kLsMaxLevels && !(gv && (std::strcmp(gv, "syncfree") == 0 ||
+                                                              std::strcmp(gv, "levels") == 0));
+        if (S->lsync) S->level_launch = false;
+    }
+    std::vector<int32_t> ls_pos, ls_lev, ls_lit;
+    if (S->lsync) {
+        for (int32_t l = 0; l < nlev; ++l) {
+            ls_lit.push_back((int32_t)ls_lev.size());
+            for (int64_t q = lptr[l]; q < lptr[l + 1]; q += kLsItem) {
+                ls_pos.push_back((int32_t)q);
+                ls_lev.push_back(l);
+            }
+        }
+        ls_lit.push_back((int32_t)ls_lev.size());
+        ls_pos.push_back((int32_t)n);
+        S->ls_nitems = (int32_t)ls_lev.size();
     }
     if ((rc = dev_upload(ctx, &S->level_ptr, lptr.data(), lptr.size())) != RSB_OK ||
         (rc = dev_upload(ctx, &S->task_row, rows.data(), rows.size())) != RSB_OK ||
@@ -442,6 +460,10 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         (single_cta && (rc = dev_upload(ctx, &S->meta, meta.data(), meta.size())) != RSB_OK) ||
         (single_cta && !unit && (rc = dev_upload(ctx, &S->ddiag, dd.data(), dd.size())) != RSB_OK) ||
         (rc = dev_alloc(ctx, (void **)&S->ticket, sizeof(unsigned long long))) != RSB_OK ||
+        (S->lsync && (rc = dev_upload(ctx, &S->ls_item_pos, ls_pos.data(), ls_pos.size())) != RSB_OK) ||
+        (S->lsync && (rc = dev_upload(ctx, &S->ls_item_level, ls_lev.data(), ls_lev.size())) != RSB_OK) ||
+        (S->lsync && (rc = dev_upload(ctx, &S->ls_level_items, ls_lit.data(), ls_lit.size())) != RSB_OK) ||
+        (S->lsync && (rc = dev_alloc(ctx, (void **)&S->ls_cnt, kLsCounters * sizeof(unsigned))) != RSB_OK) ||
         (getenv("RSB_TRSV_PROFILE") && (rc = dev_alloc(ctx, (void **)&S->prof, (8 + 4096) * sizeof(long long))) != RSB_OK)) {
         tri_free(ctx, S);
         return rc;
@@ -467,6 +489,10 @@ void tri_free(rsb_ctx *ctx, TriSched *s) {
     if (s->diag) dev_free(ctx, s->diag, padded * sizeof(double));
     dev_free(ctx, s->ticket, sizeof(unsigned long long));
     dev_free(ctx, s->level_ptr, (s->nlevels + 1) * sizeof(int32_t));
+    if (s->ls_item_pos) dev_free(ctx, s->ls_item_pos, (s->ls_nitems + 1) * sizeof(int32_t));
+    if (s->ls_item_level) dev_free(ctx, s->ls_item_level, s->ls_nitems * sizeof(int32_t));
+    if (s->ls_level_items) dev_free(ctx, s->ls_level_items, (s->nlevels + 1) * sizeof(int32_t));
+    if (s->ls_cnt) dev_free(ctx, s->ls_cnt, kLsCounters * sizeof(unsigned));
     if (s->chunk_roff) dev_free(ctx, s->chunk_roff, (s->nchunks + 1) * sizeof(int64_t));
     if (s->bpos) dev_free(ctx, s->bpos, padded * sizeof(double));
     if (s->recs) dev_free(ctx, s->recs, s->nrecs * sizeof(StageRec));

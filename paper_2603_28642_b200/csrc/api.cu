@@ -416,7 +416,8 @@ int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n) {
     RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
     RSB_TRY(get_tri(T, kind, &S));
     *variant = S->lean_n ? RSB_TRSV_LEAN
-                         : (S->single_cta ? RSB_TRSV_STAGED : (S->level_launch ? RSB_TRSV_LEVELS : RSB_TRSV_GRID));
+                         : (S->single_cta ? RSB_TRSV_STAGED
+                                          : (S->level_launch ? RSB_TRSV_LEVELS : (S->lsync ? RSB_TRSV_LSYNC : RSB_TRSV_GRID)));
     *lean_n = S->lean_n;
     return RSB_OK;
 }

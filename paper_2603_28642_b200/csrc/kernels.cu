@@ -270,21 +270,28 @@ constexpr int kSpCap = 3072;  // staged products per tile (24 KB): 12 per line
 
 __device__ __forceinline__ void stage_products(const Compressed &A, const VecIn &x, int lo, int hi,
                                                double *prod) {
-    int k = lo + threadIdx.x;
-    for (; k + 3 * kBlock < hi; k += 4 * kBlock) {
-        int c[4];
-        double v[4], xv[4];
+    // a tile holds at most kSpCap = 12 kBlock entries: two fully predicated
+    // rounds of 6 per thread, each with all its index, value and gather loads
+    // in flight together
+    constexpr int kHalf = kSpCap / kBlock / 2;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            c[u] = __ldcs(A.idx + k + u * kBlock);
-            v[u] = __ldcs(A.val + k + u * kBlock);
+    for (int h = 0; h < 2; ++h) {
+        const int k0 = lo + threadIdx.x + h * kHalf * kBlock;
+        if (k0 >= hi) break;
+        int c[kHalf];
+        double v[kHalf], xv[kHalf];
+#pragma unroll
+        for (int u = 0; u < kHalf; ++u) {
+            const int k = k0 + u * kBlock;
+            c[u] = k < hi ? __ldcs(A.idx + k) : -1;
+            v[u] = k < hi ? __ldcs(A.val + k) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = vin(x, c[u]);
+        for (int u = 0; u < kHalf; ++u) xv[u] = c[u] >= 0 ? vin(x, c[u]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) prod[k + u * kBlock - lo] = __dmul_rn(v[u], xv[u]);
+        for (int u = 0; u < kHalf; ++u)
+            if (c[u] >= 0) prod[k0 + u * kBlock - lo] = __dmul_rn(v[u], xv[u]);
     }
-    for (; k < hi; k += kBlock) prod[k - lo] = __dmul_rn(__ldcs(A.val + k), vin(x, __ldcs(A.idx + k)));
 }
 
 template <int EPI>
@@ -1155,6 +1162,8 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
             }
             if (l + 2 < (int32_t)T.h_level_ptr.size()) RSB_TRY(post_launch(ctx));
         }
+    } else if (T.lsync) {
+        RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
     } else if (T.wide) {
         k_gather_pos<<<grid_stride(T.n), kBlock, 0, ctx->stream>>>(T.n, T.n, T.task_row, a, c, v.bpos, g);
         RSB_TRY(post_launch(ctx));
@@ -1183,6 +1192,7 @@ int tri_ws_alloc(rsb_ctx *ctx, TriWs &w, int64_t cap) {
     RSB_TRY(dev_alloc(ctx, (void **)&w.bpos, (size_t)std::max<int64_t>(cap, 1) * sizeof(double)));
     w.cap = cap;
     RSB_TRY(dev_alloc(ctx, (void **)&w.ticket, sizeof(unsigned long long)));
+    RSB_TRY(dev_alloc(ctx, (void **)&w.ls_cnt, kLsCounters * sizeof(unsigned)));
     RSB_TRY_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned long long), ctx->stream));
     return RSB_OK;
 }
@@ -1190,6 +1200,7 @@ int tri_ws_alloc(rsb_ctx *ctx, TriWs &w, int64_t cap) {
 void tri_ws_free(rsb_ctx *ctx, TriWs &w) {
     if (w.bpos) dev_free(ctx, w.bpos, (size_t)std::max<int64_t>(w.cap, 1) * sizeof(double));
     if (w.ticket) dev_free(ctx, w.ticket, sizeof(unsigned long long));
+    if (w.ls_cnt) dev_free(ctx, w.ls_cnt, kLsCounters * sizeof(unsigned));
     w = TriWs{};
 }
 

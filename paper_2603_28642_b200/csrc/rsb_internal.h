@@ -181,6 +181,22 @@ struct DevBuf {
     size_t bytes = 0;
 };
 
+// level-synchronous wide solve (trsv_lsync.cu): items of up to kLsItem
+// consecutive task positions of one level, taken by persistent blocks in
+// level order; per-level done counts replicated kLsRep times
+constexpr int kLsBlock = 256;
+constexpr int kLsItem = 256;
+constexpr int kLsRep = 16;
+constexpr int kLsMaxLevels = 4096;
+struct LsyncDev {
+    int32_t nitems;
+    const int32_t *item_pos;     // nitems + 1 position bounds
+    const int32_t *item_level;   // level of each item
+    const int32_t *level_items;  // nlevels + 1: first item of each level
+    unsigned *ticket;
+    unsigned *done;              // nlevels * kLsRep
+};
+
 struct TriSched {
     int kind = -1;
     int32_t n = 0;
@@ -214,6 +230,11 @@ struct TriSched {
     // schedule unless a dot-order task has >= 16 entries (blocked BLAS order)
     int32_t max_task = 0;
     bool wide = false;
+    // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
+    bool lsync = false;
+    int32_t ls_nitems = 0;
+    int32_t *ls_item_pos = nullptr, *ls_item_level = nullptr, *ls_level_items = nullptr;
+    unsigned *ls_cnt = nullptr;  // the schedule's own counters (calls without a workspace)
     std::vector<int32_t> h_level_ptr;
     double *rval = nullptr;
     int32_t *rsrc = nullptr;
@@ -328,6 +349,9 @@ int prepare_trsv_cta(int64_t n);
 int prepare_trsv_lean(int64_t smem_bytes);
 int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
 int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g);
+int launch_trsv_lsync(rsb_ctx *ctx, const TriSched &T, const TriDev &v, unsigned *counters, VecIn a,
+                      const double *c, double *x, Gate g);
+constexpr size_t kLsCounters = 32 + (size_t)kLsMaxLevels * kLsRep;
 // one-time kernel attribute setup for the dense S solve of size s
 int prepare_chol(int64_t s);
 // one-time kernel attribute setup at context creation (dynamic shared memory)
@@ -341,6 +365,7 @@ struct TriWs {
     double *bpos = nullptr;
     int64_t cap = 0;
     unsigned long long *ticket = nullptr;
+    unsigned *ls_cnt = nullptr;  // kLsCounters
 };
 int tri_ws_alloc(rsb_ctx *ctx, TriWs &w, int64_t cap);
 void tri_ws_free(rsb_ctx *ctx, TriWs &w);

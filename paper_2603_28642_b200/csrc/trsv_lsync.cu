@@ -1,0 +1,179 @@
+// Level-synchronous grid-wide triangular solve for wide, shallow DAGs
+// (sm_100a): the config-4 structure at mu = 1 (n = 8e6: 27 / 66 levels of up
+// to 1.9M unknowns).
+//
+// Each level's task positions are cut into items of up to kLsItem
+// consecutive positions; items are numbered in level order and persistent
+// blocks take them from an atomic ticket.  A block first loads everything
+// its item needs that does not depend on the solve -- row, right-hand side
+// (the permutation gather fused), diagonal and up to N entries per task --
+// then waits until every item of the previous level has been counted done,
+// gathers the dependencies (all complete, so no per-operand polling: one
+// L2 round trip with all loads in flight), runs the reference's per-task
+// arithmetic, stores, and counts its item done.  Counts are spread over
+// kLsRep replicas per level so the completion atomics of a level's thousands
+// of items do not serialise on one address.
+//
+// Blocks hold no item while waiting for a ticket, so a block that is not
+// resident never holds up a level: no co-residency assumption, safe beside
+// concurrent solves on other streams.  The arithmetic per task is the one
+// every solve kernel here uses (sc.py:243-313 order), so results are
+// bit-identical to the other variants and to the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "rsb_internal.h"
+
+namespace rsb {
+
+namespace {
+
+__device__ __forceinline__ double vin_l(const VecIn &v, int64_t i) { return v.g ? v.p[v.g[i + v.off]] : v.p[i + v.off]; }
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int MODE, int N>
+__global__ void __launch_bounds__(kLsBlock) k_trsv_lsync(TriDev T, LsyncDev P, VecIn a, const double *c, double *x,
+                                                        Gate g) {
+    if (gated(g)) return;
+    __shared__ int s_item;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (;;) {
+        if (tid == 0) s_item = (int)atomicAdd(P.ticket, 1u);
+        __syncthreads();
+        const int it = s_item;
+        if (it >= P.nitems) return;
+        const int L = P.item_level[it];
+        const int p = P.item_pos[it] + tid;
+        const bool valid = p < P.item_pos[it + 1];
+        // ---- independent of the solve: prefetch the task
+        int row = 0, len = 0, K = 0;
+        int64_t base = 0;
+        int sl = 0;
+        double acc = 0.0, d = 1.0;
+        int cols[N];
+        double vals[N], xv[N];
+        if (valid) {
+            const int s = p >> 5;
+            sl = p & 31;
+            base = T.slice_off[s];
+            K = (int)((T.slice_off[s + 1] - base) >> 5);
+            row = T.task_row[p];
+            acc = vin_l(a, row);
+            if (c) acc = __dadd_rn(acc, c[row]);
+            if (MODE & 2) d = T.diag[p];
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            cols[q] = -1;
+            vals[q] = 0.0;
+            xv[q] = 0.0;
+            if (q < K) {
+                cols[q] = __ldcs(T.ecol + base + (int64_t)q * 32 + sl);
+                vals[q] = __ldcs(T.eval + base + (int64_t)q * 32 + sl);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) len += cols[q] >= 0;
+        // ---- wait until the previous level is complete
+        if (L > 0 && tid < 32) {
+            const unsigned want = (unsigned)(P.level_items[L] - P.level_items[L - 1]);
+            const unsigned *cnt = P.done + (size_t)(L - 1) * kLsRep;
+            for (;;) {
+                unsigned v = lane < kLsRep ? ld_acquire_u32(cnt + lane) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (v >= want) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        if (valid) {
+            // every dependency is final: all gathers of the task in flight at once
+#pragma unroll
+            for (int q = 0; q < N; ++q)
+                if (cols[q] >= 0) xv[q] = __ldcg(x + cols[q]);
+            double r = acc;
+            if (!(MODE & 1)) {
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (q < len && xv[q] != 0.0) r = __dsub_rn(r, __dmul_rn(vals[q], xv[q]));
+                if (len == N)  // entries continue past the registers (rare)
+                    for (int q = N; q < K; ++q) {
+                        const int64_t e = base + (int64_t)q * 32 + sl;
+                        const int col = T.ecol[e];
+                        if (col < 0) break;
+                        const double xj = __ldcg(x + col);
+                        if (xj != 0.0) r = __dsub_rn(r, __dmul_rn(T.eval[e], xj));
+                    }
+            } else {  // < 16 entries: the scalar OpenBLAS order (checked at analysis)
+                double dot = 0.0;
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (q < len) dot = fma(vals[q], xv[q], dot);
+                if (len == N)
+                    for (int q = N; q < K; ++q) {
+                        const int64_t e = base + (int64_t)q * 32 + sl;
+                        const int col = T.ecol[e];
+                        if (col < 0) break;
+                        dot = fma(T.eval[e], __ldcg(x + col), dot);
+                    }
+                r = __dsub_rn(r, dot);
+            }
+            if (MODE & 2) r = __ddiv_rn(r, d);
+            x[row] = r;
+        }
+        // ---- count the item done (the barrier orders the block's stores
+        // before thread 0's release)
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(P.done + (size_t)L * kLsRep + (it % kLsRep), 1u);
+        }
+    }
+}
+
+using LsyncKernel = void (*)(TriDev, LsyncDev, VecIn, const double *, double *, Gate);
+
+template <int MODE>
+LsyncKernel lsync_kernel(int n) {
+    if (n <= 4) return k_trsv_lsync<MODE, 4>;
+    if (n <= 8) return k_trsv_lsync<MODE, 8>;
+    return k_trsv_lsync<MODE, 12>;
+}
+
+}  // namespace
+
+int launch_trsv_lsync(rsb_ctx *ctx, const TriSched &T, const TriDev &v, unsigned *counters, VecIn a,
+                      const double *c, double *x, Gate g) {
+    LsyncKernel k;
+    switch (T.mode) {
+        case 0: k = lsync_kernel<0>(T.max_task); break;
+        case 1: k = lsync_kernel<1>(T.max_task); break;
+        case 2: k = lsync_kernel<2>(T.max_task); break;
+        default: k = lsync_kernel<3>(T.max_task); break;
+    }
+    static int occ_cache[4][3] = {};
+    const int ni = T.max_task <= 4 ? 0 : (T.max_task <= 8 ? 1 : 2);
+    int &occ = occ_cache[T.mode & 3][ni];
+    if (occ == 0) {
+        RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kLsBlock, 0));
+        occ = std::max(occ, 1);
+    }
+    int sms = 0;
+    RSB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    // counters: [0] ticket, [32 ..) per-level replicated done counts
+    const LsyncDev P{T.ls_nitems, T.ls_item_pos, T.ls_item_level, T.ls_level_items, counters, counters + 32};
+    RSB_TRY_CUDA(cudaMemsetAsync(counters, 0, (32 + (size_t)T.nlevels * kLsRep) * sizeof(unsigned), ctx->stream));
+    const int grid = (int)std::min<int64_t>((int64_t)sms * occ, T.ls_nitems);
+    k<<<std::max(grid, 1), kLsBlock, 0, ctx->stream>>>(v, P, a, c, x, g);
+    return RSB_OK;
+}
+
+}  // namespace rsb
