@@ -426,17 +426,17 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         if (gv && std::strcmp(gv, "levels") == 0) S->level_launch = true;
         if (gv && std::strcmp(gv, "syncfree") == 0) S->level_launch = false;
         S->h_level_ptr = lptr;
-        // level-synchronous items (trsv_lsync.cu): the default for wide DAGs of
-        // at most kLsMaxLevels levels
-        S->lsync = S->wide && nlev <= kLsMaxLevels && !(gv && (std::strcmp(gv, "syncfree") == 0 ||
-                                                              std::strcmp(gv, "levels") == 0));
+        // level-synchronous items (trsv_lsync.cu, RSB_TRSV_GRID=lsync) for wide
+        // DAGs of at most kLsMaxLevels levels
+        S->lsync = S->wide && nlev <= kLsMaxLevels && gv && std::strcmp(gv, "lsync") == 0;
         if (S->lsync) S->level_launch = false;
     }
     std::vector<int32_t> ls_pos, ls_lev, ls_lit;
     if (S->lsync) {
         for (int32_t l = 0; l < nlev; ++l) {
             ls_lit.push_back((int32_t)ls_lev.size());
-            for (int64_t q = lptr[l]; q < lptr[l + 1]; q += kLsItem) {
+            // items end on slice boundaries (a warp's item is one slice's lanes)
+            for (int64_t q = lptr[l]; q < lptr[l + 1]; q = (q / kLsItem + 1) * kLsItem) {
                 ls_pos.push_back((int32_t)q);
                 ls_lev.push_back(l);
             }

@@ -182,11 +182,11 @@ struct DevBuf {
 };
 
 // level-synchronous wide solve (trsv_lsync.cu): items of up to kLsItem
-// consecutive task positions of one level, taken by persistent blocks in
+// consecutive task positions of one level, taken by persistent warps in
 // level order; per-level done counts replicated kLsRep times
 constexpr int kLsBlock = 256;
-constexpr int kLsItem = 256;
-constexpr int kLsRep = 16;
+constexpr int kLsItem = 32;
+constexpr int kLsRep = 32;
 constexpr int kLsMaxLevels = 4096;
 struct LsyncDev {
     int32_t nitems;

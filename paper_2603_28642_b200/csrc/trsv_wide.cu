@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "rsb_internal.h"
@@ -53,39 +54,83 @@ __device__ __forceinline__ void st_relaxed_f64(double *p, double v) {
 
 __device__ __forceinline__ bool is_sentinel(double v) { return __double_as_longlong(v) == (long long)kSentinel; }
 
-// entries past N (rare): are all of them published? (never blocks: a
-// dependency may sit in another lane of the same warp)
+// Entries past the N held in registers (U at mu = 1: ~10% of the rows have
+// more than 12 entries, so most slices hold one).  They are handled in
+// batches of kTailB with every load of a batch in flight together: a long
+// task costs ceil((len - N) / kTailB) round trips instead of len - N.
+constexpr int kTailB = 8;
+
+// the task's entry count past `from` (entries are contiguous, then -1 padding)
+__device__ __noinline__ int wide_tail_len(const TriDev &T, int64_t base, int lane, int from, int K) {
+    int len = from;
+    for (int q0 = from; q0 < K; q0 += kTailB) {
+        int col[kTailB];
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) col[u] = q0 + u < K ? T.ecol[base + (int64_t)(q0 + u) * 32 + lane] : -1;
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) len += col[u] >= 0;
+        if (col[kTailB - 1] < 0) break;
+    }
+    return len;
+}
+
+// are all entries past `from` published? (never blocks: a dependency may sit
+// in another lane of the same warp)
 __device__ __noinline__ bool wide_tail_ready(const TriDev &T, int64_t base, int lane, int from, int len,
                                              const double *x) {
-    for (int q = from; q < len; ++q)
-        if (is_sentinel(ld_relaxed_f64(x + T.ecol[base + (int64_t)q * 32 + lane]))) return false;
+    for (int q0 = from; q0 < len; q0 += kTailB) {
+        int col[kTailB];
+        unsigned long long v[kTailB];
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) col[u] = q0 + u < len ? T.ecol[base + (int64_t)(q0 + u) * 32 + lane] : -1;
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) {
+            v[u] = 0;
+            poll_if(col[u] >= 0, x + (col[u] >= 0 ? col[u] : 0), v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u)
+            if (col[u] >= 0 && v[u] == kSentinel) return false;
+    }
     return true;
 }
 
-// entries past N (rare), all published: the sequential order, out of line
+// entries past `from`, all published: the sequential order, out of line
 template <int MODE>
 __device__ __noinline__ double wide_tail(const TriDev &T, int64_t base, int lane, int from, int len, double acc,
                                          double dot, const double *x) {
-    for (int q = from; q < len; ++q) {
-        const int64_t e = base + (int64_t)q * 32 + lane;
-        const int col = T.ecol[e];
-        const double v = T.eval[e];
-        double xj;
-        do {
-            xj = ld_relaxed_f64(x + col);
-        } while (is_sentinel(xj));
-        if (!(MODE & 1)) {
-            if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(v, xj));
-        } else {
-            dot = fma(v, xj, dot);
+    for (int q0 = from; q0 < len; q0 += kTailB) {
+        int col[kTailB];
+        double val[kTailB];
+        unsigned long long v[kTailB];
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) {
+            const bool in = q0 + u < len;
+            col[u] = in ? T.ecol[base + (int64_t)(q0 + u) * 32 + lane] : -1;
+            val[u] = in ? T.eval[base + (int64_t)(q0 + u) * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) {
+            v[u] = 0;
+            poll_if(col[u] >= 0, x + (col[u] >= 0 ? col[u] : 0), v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kTailB; ++u) {
+            if (col[u] < 0) break;
+            const double xj = __longlong_as_double((long long)v[u]);
+            if (!(MODE & 1)) {
+                if (xj != 0.0) acc = __dsub_rn(acc, __dmul_rn(val[u], xj));
+            } else {
+                dot = fma(val[u], xj, dot);
+            }
         }
     }
     return (MODE & 1) ? __dsub_rn(acc, dot) : acc;
 }
 
-template <int MODE, int N>
+template <int MODE, int N, bool TAIL>
 __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
-                                                          Gate g) {
+                                                          unsigned max_backoff, Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
     auto take = [&]() {
@@ -131,8 +176,8 @@ __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const dou
                     need |= 1u << q;
                     ++len;
                 }
-            if (len == N)  // entries continue past the registers
-                while (len < K && T.ecol[base + (int64_t)len * 32 + lane] >= 0) ++len;
+            if (TAIL && len == N && K > N)  // entries continue past the registers
+                len = wide_tail_len(T, base, lane, N, K);
         }
         bool done = !valid;
         // warp-synchronous polling: every round each pending lane loads all
@@ -143,7 +188,7 @@ __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const dou
         while (__any_sync(0xffffffffu, !done)) {
             if (__all_sync(0xffffffffu, done || need == prev_need) && backoff) __nanosleep(backoff);
             prev_need = need;
-            backoff = backoff ? min(backoff * 2, kWideMaxBackoffNs) : kWideMinBackoffNs;
+            backoff = backoff ? min(backoff * 2, max_backoff) : kWideMinBackoffNs;
             if (!done) {
                 unsigned long long pv[N];
 #pragma unroll
@@ -157,19 +202,19 @@ __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const dou
                         xv[q] = __longlong_as_double((long long)pv[q]);
                         need &= ~(1u << q);
                     }
-                if (need == 0 && (len <= N || wide_tail_ready(T, base, lane, N, len, x))) {
+                if (need == 0 && (!TAIL || len <= N || wide_tail_ready(T, base, lane, N, len, x))) {
                     double r = acc;
                     if (!(MODE & 1)) {
 #pragma unroll
                         for (int q = 0; q < N; ++q)
                             if (q < len && xv[q] != 0.0) r = __dsub_rn(r, __dmul_rn(vals[q], xv[q]));
-                        if (len > N) r = wide_tail<MODE>(T, base, lane, N, len, r, 0.0, x);
+                        if (TAIL && len > N) r = wide_tail<MODE>(T, base, lane, N, len, r, 0.0, x);
                     } else if (len > 0) {  // < 16 entries (the scalar OpenBLAS order; checked at analysis)
                         double dot = 0.0;
 #pragma unroll
                         for (int q = 0; q < N; ++q)
                             if (q < len) dot = fma(vals[q], xv[q], dot);
-                        r = (len > N) ? wide_tail<MODE>(T, base, lane, N, len, r, dot, x) : __dsub_rn(r, dot);
+                        r = (TAIL && len > N) ? wide_tail<MODE>(T, base, lane, N, len, r, dot, x) : __dsub_rn(r, dot);
                     }
                     if (MODE & 2) r = __ddiv_rn(r, d);
                     if (row >= 0) st_relaxed_f64(x + row, r);
@@ -182,13 +227,14 @@ __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const dou
     }
 }
 
-using WideKernel = void (*)(TriDev, const double *, double *, int, Gate);
+using WideKernel = void (*)(TriDev, const double *, double *, int, unsigned, Gate);
 
 template <int MODE>
 WideKernel wide_kernel(int n) {
-    if (n <= 4) return k_trsv_wide<MODE, 4>;
-    if (n <= 8) return k_trsv_wide<MODE, 8>;
-    return k_trsv_wide<MODE, 12>;
+    if (n <= 4) return k_trsv_wide<MODE, 4, false>;
+    if (n <= 8) return k_trsv_wide<MODE, 8, false>;
+    if (n <= 12) return k_trsv_wide<MODE, 12, false>;
+    return k_trsv_wide<MODE, 12, true>;
 }
 
 WideKernel wide_kernel_for(int mode, int n) {
@@ -204,8 +250,8 @@ WideKernel wide_kernel_for(int mode, int n) {
 
 int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g) {
     WideKernel k = wide_kernel_for(T.mode, T.max_task);
-    static int per_sm[4][3] = {};  // occupancy of each instantiation, queried once
-    const int ni = T.max_task <= 4 ? 0 : (T.max_task <= 8 ? 1 : 2);
+    static int per_sm[4][4] = {};  // occupancy of each instantiation, queried once
+    const int ni = T.max_task <= 4 ? 0 : (T.max_task <= 8 ? 1 : (T.max_task <= 12 ? 2 : 3));
     int &occ = per_sm[T.mode & 3][ni];
     if (occ == 0) {
         RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWideBlock, 0));
@@ -214,8 +260,13 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const dou
     int sms = 0;
     RSB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
     const int nslices = (T.n + 31) / 32;
-    const int grid = (int)std::min<int64_t>((int64_t)sms * occ, (nslices * 32 + kWideBlock - 1) / kWideBlock);
-    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, bpos, x, nslices, g);
+    // experiments: RSB_WIDE_OCC caps the resident blocks per SM, RSB_WIDE_BACKOFF
+    // sets the longest back-off (ns) of a waiting warp
+    const char *eo = getenv("RSB_WIDE_OCC"), *eb = getenv("RSB_WIDE_BACKOFF");
+    const int use_occ = eo ? std::max(1, std::min(occ, atoi(eo))) : occ;
+    const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
+    const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ, (nslices * 32 + kWideBlock - 1) / kWideBlock);
+    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, bpos, x, nslices, max_backoff, g);
     return RSB_OK;
 }
 

@@ -123,12 +123,12 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
     assert check(M, L.TRI_LOWER_UNIT, b, monkeypatch)[0] in ("staged", "grid", "levels")
     W = leveled_lower([6000] * 5, 4, rng)
     bw = rng.standard_normal(W.ncols)
-    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "lsync"
-    # the sync-free persistent kernel on the same DAG
+    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+    # the level-synchronous persistent kernel on the same DAG
     with monkeypatch.context() as m:
-        m.setenv("RSB_TRSV_GRID", "syncfree")
+        m.setenv("RSB_TRSV_GRID", "lsync")
         W1 = P.CscMatrix(W.nrows, W.ncols, W.col_ptr.copy(), W.row_idx.copy(), W.values.copy())
-        assert check(W1, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+        assert check(W1, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "lsync"
     # a grid launch per level on the same DAG
     with monkeypatch.context() as m:
         m.setenv("RSB_TRSV_GRID", "levels")
@@ -139,12 +139,12 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
 @pytest.mark.parametrize("grid", ["lsync", "syncfree"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
-    """The persistent wide solves (grid schedules): level-synchronous (the
-    default) and sync-free.  Tasks past the register entries take the
+    """The persistent wide solves (grid schedules): sync-free (the default)
+    and level-synchronous.  Tasks past the register entries take the
     out-of-line tail (sequential order); the sync-free kernel waits for it
     without blocking (a dependency may sit in another lane of the warp)."""
-    if grid == "syncfree":
-        monkeypatch.setenv("RSB_TRSV_GRID", "syncfree")
+    if grid == "lsync":
+        monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
     rng = np.random.default_rng(100 + k)
     Ms = leveled_lower([5000] * 4, k, rng, window=4000)  # strictly lower: the unit kinds
     b = rng.standard_normal(Ms.ncols)
