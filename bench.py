@@ -398,6 +398,8 @@ def run_b200(args):
     achieved = (tbytes * K) / (tri_ms[0] / 1e3) / 1e9
     peak, peak_kind = measured_peak()
     traffic, traffic_src = ncu_traffic()
+    if not (args.config == 1 and args.grid == 256 and args.mu == 1.0 and mode == "cg"):
+        traffic, traffic_src = None, "no ncu capture committed for this workload"
     cpu = None
     if world == 1:
         rate, kc, dtc = cpu_oracle_rate(S, pre, b, norm_a, args.cpu_seconds)

@@ -151,6 +151,16 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         std::vector<int64_t> pos(lstart.begin(), lstart.end() - 1);
         for (int64_t t = 0; t < n; ++t) order[pos[level[t]]++] = (int32_t)t;
     }
+    // Wide DAGs (grid schedules): inside a level the order is free (its tasks
+    // are independent), so put the longest tasks first.  Long tasks then share
+    // slices -- a slice waits for its longest lane -- and start earliest.
+    if (!(n <= kCtaTriMaxN && n / std::max<int64_t>(1, nlev) <= kCtaTriMaxMeanWidth) &&
+        !(getenv("RSB_TRSV_SORT") && std::strcmp(getenv("RSB_TRSV_SORT"), "0") == 0)) {
+        for (int32_t l = 0; l < nlev; ++l)
+            std::stable_sort(order.begin() + lstart[l], order.begin() + lstart[l + 1], [&](int32_t a, int32_t b) {
+                return tptr[a + 1] - tptr[a] > tptr[b + 1] - tptr[b];
+            });
+    }
 
     // warp-interleaved packing: slice widths
     const int64_t nslices = (n + 31) / 32;
@@ -414,6 +424,20 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         int64_t ml = 0;
         for (int64_t t = 0; t < n; ++t) ml = std::max(ml, tptr[t + 1] - tptr[t]);
         S->max_task = (int32_t)ml;
+        // the wide kernel's register entries: the smallest of 4 / 8 / 12 that
+        // holds at least 94% of the tasks (the rest take the batched tail)
+        {
+            int64_t le4 = 0, le8 = 0;
+            for (int64_t t = 0; t < n; ++t) {
+                const int64_t len = tptr[t + 1] - tptr[t];
+                le4 += len <= 4;
+                le8 += len <= 8;
+            }
+            S->wide_n = (ml <= 4 || le4 >= n * 94 / 100) ? 4 : ((ml <= 8 || le8 >= n * 94 / 100) ? 8 : 12);
+            if (is_dot && ml >= S->wide_n) S->wide_n = 12;  // dot-order tasks: the tail keeps the scalar chain (< 16)
+            const char *wn = getenv("RSB_WIDE_N");  // experiments
+            if (wn) S->wide_n = std::max(4, std::min(12, atoi(wn))) <= 4 ? 4 : (atoi(wn) <= 8 ? 8 : 12);
+        }
         const char *wv = getenv("RSB_TRSV_WIDE");  // "0": the previous grid kernel (experiments)
         S->wide = !single_cta && !(is_dot && ml >= 16) && !(wv && std::strcmp(wv, "0") == 0);
     }

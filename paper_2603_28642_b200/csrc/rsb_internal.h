@@ -229,6 +229,7 @@ struct TriSched {
     // longest task; the persistent wide kernel (trsv_wide.cu) runs the grid
     // schedule unless a dot-order task has >= 16 entries (blocked BLAS order)
     int32_t max_task = 0;
+    int32_t wide_n = 12;  // entries per task the wide kernel holds in registers (4, 8 or 12)
     bool wide = false;
     // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
     bool lsync = false;

@@ -128,8 +128,15 @@ __device__ __noinline__ double wide_tail(const TriDev &T, int64_t base, int lane
     return (MODE & 1) ? __dsub_rn(acc, dot) : acc;
 }
 
+// resident blocks the register budget is sized for: fewer registers per task
+// (smaller N) buy more warps in flight, which is what the solve is bound by
+template <int N>
+struct WideOcc {
+    static constexpr int value = N <= 4 ? 6 : (N <= 8 ? 4 : 3);
+};
+
 template <int MODE, int N, bool TAIL>
-__global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
+__global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
                                                           unsigned max_backoff, Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
@@ -230,29 +237,31 @@ __global__ void __launch_bounds__(kWideBlock, 3) k_trsv_wide(TriDev T, const dou
 using WideKernel = void (*)(TriDev, const double *, double *, int, unsigned, Gate);
 
 template <int MODE>
-WideKernel wide_kernel(int n) {
-    if (n <= 4) return k_trsv_wide<MODE, 4, false>;
-    if (n <= 8) return k_trsv_wide<MODE, 8, false>;
-    if (n <= 12) return k_trsv_wide<MODE, 12, false>;
-    return k_trsv_wide<MODE, 12, true>;
+WideKernel wide_kernel(int n, bool tail) {
+    if (n <= 4) return tail ? k_trsv_wide<MODE, 4, true> : k_trsv_wide<MODE, 4, false>;
+    if (n <= 8) return tail ? k_trsv_wide<MODE, 8, true> : k_trsv_wide<MODE, 8, false>;
+    return tail ? k_trsv_wide<MODE, 12, true> : k_trsv_wide<MODE, 12, false>;
 }
 
-WideKernel wide_kernel_for(int mode, int n) {
+WideKernel wide_kernel_for(int mode, int n, bool tail) {
     switch (mode) {
-        case 0: return wide_kernel<0>(n);
-        case 1: return wide_kernel<1>(n);
-        case 2: return wide_kernel<2>(n);
-        default: return wide_kernel<3>(n);
+        case 0: return wide_kernel<0>(n, tail);
+        case 1: return wide_kernel<1>(n, tail);
+        case 2: return wide_kernel<2>(n, tail);
+        default: return wide_kernel<3>(n, tail);
     }
 }
 
 }  // namespace
 
 int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g) {
-    WideKernel k = wide_kernel_for(T.mode, T.max_task);
-    static int per_sm[4][4] = {};  // occupancy of each instantiation, queried once
-    const int ni = T.max_task <= 4 ? 0 : (T.max_task <= 8 ? 1 : (T.max_task <= 12 ? 2 : 3));
-    int &occ = per_sm[T.mode & 3][ni];
+    // registers hold wide_n entries per task (most tasks fit);
+    // longer tasks take the batched out-of-line tail
+    const bool tail = T.max_task > T.wide_n;
+    WideKernel k = wide_kernel_for(T.mode, T.wide_n, tail);
+    static int per_sm[4][3][2] = {};  // occupancy of each instantiation, queried once
+    const int ni = T.wide_n <= 4 ? 0 : (T.wide_n <= 8 ? 1 : 2);
+    int &occ = per_sm[T.mode & 3][ni][tail ? 1 : 0];
     if (occ == 0) {
         RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWideBlock, 0));
         occ = std::max(occ, 1);
