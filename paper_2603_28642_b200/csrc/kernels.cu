@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv_tile(Compressed A, VecIn x, dou
     y[i] = acc;
 }
 
-template <int EPI>
-__global__ void __launch_bounds__(kBlock, 4) k_spmv_t_tile(Compressed At, VecIn y, double *z, VecIn e, Gate g) {
+template <int EPI, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmv_t_tile(Compressed At, VecIn y, double *z, VecIn e, Gate g) {
     if (gated(g)) return;
     __shared__ double prod[kSpCap];
     const int64_t l0 = blockIdx.x * (int64_t)kBlock;
@@ -1066,19 +1066,25 @@ inline int post_launch(rsb_ctx *ctx, int kernels = 1) {
 
 }  // namespace
 
-// RSB_SPMV=thread selects the thread-per-line kernels (experiments)
-static bool spmv_tiled() {
-    static const int tiled = [] {
+// RSB_SPMV=thread / tile forces the thread-per-line / tiled kernels (experiments)
+static int spmv_force() {
+    static const int force = [] {
         const char *v = getenv("RSB_SPMV");
-        return (v && strcmp(v, "thread") == 0) ? 0 : 1;
+        return v ? (strcmp(v, "thread") == 0 ? 1 : (strcmp(v, "tile") == 0 ? 2 : 0)) : 0;
     }();
-    return tiled != 0;
+    return force;
 }
+static bool spmv_tiled() { return spmv_force() != 1; }
 
 int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
     if (A.nlines == 0) return RSB_OK;
     const int grid = grid_for(A.nlines, kBlock);
-    if (spmv_tiled()) {
+    // rows of at most 8 entries (A of configs 0 / 4: 6 per row): one thread per
+    // row keeps the loads of a warp's rows in the same few lines and measured
+    // faster (config 4 at n = 8e6: 0.55 vs 0.66 ms); longer or uneven rows
+    // take the tiled kernel
+    const bool tiled = spmv_force() == 2 || (spmv_tiled() && A.max_len > 8);
+    if (tiled) {
         switch (epi) {
             case EPI_STORE: k_spmv_tile<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
             case EPI_ADD: k_spmv_tile<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
@@ -1098,10 +1104,17 @@ int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int ep
     if (At.nlines == 0) return RSB_OK;
     const int grid = grid_for(At.nlines, kBlock);
     if (spmv_tiled()) {
-        if (epi == EPI_ADD)
-            k_spmv_t_tile<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
-        else
-            k_spmv_t_tile<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        static const bool occ6 = getenv("RSB_SPMV_T_OCC") && atoi(getenv("RSB_SPMV_T_OCC")) == 6;  // experiments
+        if (occ6) {
+            if (epi == EPI_ADD)
+                k_spmv_t_tile<EPI_ADD, 6><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+            else
+                k_spmv_t_tile<EPI_STORE, 6><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        } else if (epi == EPI_ADD) {
+            k_spmv_t_tile<EPI_ADD, 4><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        } else {
+            k_spmv_t_tile<EPI_STORE, 4><<<grid, kBlock, 0, ctx->stream>>>(At, y, z, e, g);
+        }
         return post_launch(ctx);
     }
     if (epi == EPI_ADD)

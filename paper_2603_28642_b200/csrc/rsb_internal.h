@@ -110,6 +110,7 @@ struct Compressed {
     const int32_t *ptr;
     const int32_t *idx;
     const double *val;
+    int32_t max_len;  // longest line
 };
 
 // A vector operand, optionally read through a gather: v(i) = p[g[i + off]]
@@ -313,10 +314,10 @@ struct rsb_mat {
     std::vector<double> h_val;
     rsb::TriSched *tri[6] = {};
     rsb::Compressed csr() const {
-        return rsb::Compressed{(int32_t)nrows, (int32_t)ncols, nnz, r_ptr, r_idx, r_val};
+        return rsb::Compressed{(int32_t)nrows, (int32_t)ncols, nnz, r_ptr, r_idx, r_val, max_row_len};
     }
     rsb::Compressed csc() const {
-        return rsb::Compressed{(int32_t)ncols, (int32_t)nrows, nnz, c_ptr, c_idx, c_val};
+        return rsb::Compressed{(int32_t)ncols, (int32_t)nrows, nnz, c_ptr, c_idx, c_val, max_col_len};
     }
 };
 

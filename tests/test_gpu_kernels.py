@@ -181,3 +181,42 @@ def test_device_dot_reference_order(n):
     out = np.zeros(1)
     L.check(L.lib().rsb_dot(get_context().h, n, L.ptr(a), L.ptr(b), out.ctypes.data_as(L.f64p), L.RSB_HOST))
     assert out[0] == O.dot(a, b)
+
+
+_SPMV_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+import paper_2603_28642_b200 as P
+from paper_2603_28642_b200 import workloads as W
+from conftest import csc_from, golden
+from oracle import oracle as O
+K = golden("kernels.npz")
+mats = []
+c = 0
+while f"mv{{c}}_shape" in K:
+    mats.append(csc_from(K, f"mv{{c}}")); c += 1
+mats.append(W.config4(seed=4, n=5000, nrhs=0)[0])
+mats.append(W.config2(seed=2, n=3000)[0])
+rng = np.random.default_rng(7)
+for A in mats:
+    x, y = rng.standard_normal(A.ncols), rng.standard_normal(A.nrows)
+    assert np.array_equal(P.matvec(A, x), O.matvec(A, x))
+    assert np.array_equal(P.matvec_transpose(A, y), O.matvec_transpose(A, y))
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("variant", ["tile", "thread"])
+def test_spmv_forced_variants_bitwise(variant):
+    """Both SpMV kernel families (tiled / thread per line, RSB_SPMV) on the
+    golden matrices, config 4 (6 entries per row) and config 2 (dense rows
+    past the tile's staging buffer)."""
+    import os
+    import subprocess
+    import sys
+
+    tests = os.path.dirname(os.path.abspath(__file__))
+    script = _SPMV_VARIANT_SCRIPT.format(repo=os.path.dirname(tests), tests=tests)
+    r = subprocess.run([sys.executable, "-c", script], env=dict(os.environ, RSB_SPMV=variant),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
