@@ -437,12 +437,13 @@ int enqueue_iteration(rsb_solver *S) {
     RSB_TRY(chk(ctx));
     RSB_TRY(launch_axpy(ctx, S->x, S->p, &st->alpha, +1, n, g));
     RSB_TRY(launch_axpy(ctx, S->r, S->q, &st->alpha, -1, m, g));
-    // ||x|| with the estimator, and z.z, only decide whether to stop: they run
-    // on a side branch of the graph beside A^T r and the preconditioner
-    // application.  Those are gated on the status the estimator sets, so an
-    // application started before a stop is merely wasted; k_it_zz runs after
-    // the join, keeping the reference's order of the two stopping checks
-    // (sv.py:229-237).  (Not in tree-dot mode, whose dots share one scratch.)
+    // The preconditioner application reads only r (sv.py:238), so it runs on
+    // the main branch while a side branch computes ||x|| with the estimator,
+    // then z = A^T r and z.z (sv.py:220-237).  Everything is gated on the
+    // status the estimator sets, so an application started before a stop is
+    // merely wasted (z is not an output); k_it_zz runs after the join, keeping
+    // the reference's order of the stopping checks.  (Not in tree-dot mode,
+    // whose dots share one scratch.)
     const bool fork = !(ctx->flags & RSB_DOT_TREE) && ctx->side;
     auto on_side = [&](auto &&launches) -> int {
         cudaStream_t main = ctx->stream;
@@ -451,36 +452,30 @@ int enqueue_iteration(rsb_solver *S) {
         ctx->stream = main;
         return rc;
     };
-    if (fork) {
-        RSB_TRY_CUDA(cudaEventRecord(ctx->fork_ev[0], ctx->stream));
-        RSB_TRY_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[0], 0));
-    }
-    auto norm_and_estimate = [&]() -> int {
+    auto side_branch = [&]() -> int {
         RSB_TRY(launch_dot(ctx, n, VecIn{S->x, nullptr, 0}, VecIn{S->x, nullptr, 0}, &st->xnorm, 1, g, nullptr));
         k_it_estimate<<<1, 1, 0, ctx->stream>>>(st, S->alphas, S->sigmas, S->x_norms, S->history);
-        return chk(ctx);
-    };
-    RSB_TRY(fork ? on_side(norm_and_estimate) : norm_and_estimate());
-    RSB_TRY(launch_spmv_t(ctx, S->A->csc(), VecIn{S->r, nullptr, 0}, S->z, EPI_STORE, VecIn{}, g));
-    auto zz_dot = [&]() -> int {
+        RSB_TRY(chk(ctx));
+        RSB_TRY(launch_spmv_t(ctx, S->A->csc(), VecIn{S->r, nullptr, 0}, S->z, EPI_STORE, VecIn{}, g));
         return launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->z, nullptr, 0}, &st->zz, 0, g, nullptr);
     };
     if (fork) {
-        RSB_TRY_CUDA(cudaEventRecord(ctx->fork_ev[1], ctx->stream));
-        RSB_TRY_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[1], 0));
-        RSB_TRY(on_side(zz_dot));
+        RSB_TRY_CUDA(cudaEventRecord(ctx->fork_ev[0], ctx->stream));
+        RSB_TRY_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[0], 0));
+        RSB_TRY(on_side(side_branch));
         RSB_TRY_CUDA(cudaEventRecord(ctx->fork_ev[2], ctx->side));
     } else {
-        RSB_TRY(zz_dot());
+        RSB_TRY(side_branch());
         k_it_zz<<<1, 1, 0, ctx->stream>>>(st);
         RSB_TRY(chk(ctx));
     }
-    RSB_TRY(enqueue_precondition(S, g));
+    if (S->pre) RSB_TRY(enqueue_precondition(S, g));
     if (fork) {
         RSB_TRY_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->fork_ev[2], 0));
         k_it_zz<<<1, 1, 0, ctx->stream>>>(st);
         RSB_TRY(chk(ctx));
     }
+    if (!S->pre) RSB_TRY(enqueue_precondition(S, g));  // plain CGLS: h = z, after the branch that computes z
     RSB_TRY(launch_dot(ctx, n, VecIn{S->z, nullptr, 0}, VecIn{S->h, nullptr, 0}, &st->zh, 0, g, nullptr));
     k_it_beta<<<1, 1, 0, ctx->stream>>>(st);
     RSB_TRY(chk(ctx));
