@@ -137,7 +137,7 @@ struct WideOcc {
 
 template <int MODE, int N, bool TAIL>
 __global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
-                                                          unsigned max_backoff, Gate g) {
+                                                          unsigned max_backoff, int EARLY, Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
     auto take = [&]() {
@@ -151,13 +151,23 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(Tri
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
         T.prof[7] = (long long)ts;
     }
+    // Optional software pipelining over slices (EARLY): the next slice's
+    // ticket is taken while this slice's task loads are in flight, and its
+    // entry offsets are loaded while this slice polls.  Holding the next
+    // ticket cannot deadlock (it is started after the current slice, whose
+    // dependencies all precede it), but measured slower: the held slice
+    // waits behind the current one instead of being taken by a free warp.
+    int64_t base = 0, base_end = 0;
+    if (s < nslices) {
+        base = T.slice_off[s];
+        base_end = T.slice_off[s + 1];
+    }
     while (s < nslices) {
-        // (no early ticket: a slice held while the warp works on another is
-        // never ready-and-loaded when its level is reached)
+        int nxt_raw = 0;
+        if (EARLY && lane == 0) nxt_raw = (int)atomicAdd(T.ticket, 1ull);
         const int t = s * 32 + lane;
         const bool valid = t < T.n;
-        const int64_t base = T.slice_off[s];
-        const int K = (int)((T.slice_off[s + 1] - base) >> 5);
+        const int K = (int)((base_end - base) >> 5);
         int row = -1, len = 0;
         double acc = 0.0, d = 1.0;
         int cols[N];
@@ -185,6 +195,15 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(Tri
                 }
             if (TAIL && len == N && K > N)  // entries continue past the registers
                 len = wide_tail_len(T, base, lane, N, K);
+        }
+        int nxt = 0;
+        int64_t nbase = 0, nbase_end = 0;
+        if (EARLY) {
+            nxt = __shfl_sync(0xffffffffu, nxt_raw, 0);
+            if (nxt < nslices) {
+                nbase = T.slice_off[nxt];
+                nbase_end = T.slice_off[nxt + 1];
+            }
         }
         bool done = !valid;
         // warp-synchronous polling: every round each pending lane loads all
@@ -230,11 +249,21 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(Tri
             }
             __syncwarp();
         }
-        s = take();
+        if (EARLY) {
+            s = nxt;
+            base = nbase;
+            base_end = nbase_end;
+        } else {
+            s = take();
+            if (s < nslices) {
+                base = T.slice_off[s];
+                base_end = T.slice_off[s + 1];
+            }
+        }
     }
 }
 
-using WideKernel = void (*)(TriDev, const double *, double *, int, unsigned, Gate);
+using WideKernel = void (*)(TriDev, const double *, double *, int, unsigned, int, Gate);
 
 template <int MODE>
 WideKernel wide_kernel(int n, bool tail) {
@@ -275,7 +304,12 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const dou
     const int use_occ = eo ? std::max(1, std::min(occ, atoi(eo))) : occ;
     const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
     const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ, (nslices * 32 + kWideBlock - 1) / kWideBlock);
-    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, bpos, x, nslices, max_backoff, g);
+    // RSB_WIDE_EARLY=1: software pipelining over slices (experiments; measured
+    // slower on config 4 at n = 2e6: U 0.45 vs 0.30 ms -- a warp holding its
+    // next slice delays that slice behind its current one)
+    const char *ee = getenv("RSB_WIDE_EARLY");
+    const int early = (ee && atoi(ee) == 1) ? 1 : 0;
+    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, bpos, x, nslices, max_backoff, early, g);
     return RSB_OK;
 }
 

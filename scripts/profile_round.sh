@@ -26,6 +26,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 # the first timed iteration's 8 solves: 1 apply at start + 3 warm-up iterations precede it
 ncu --set full --clock-control none --import-source on -k regex:k_trsv -s 32 -c 8 -o $O/trsv_$R -f $SHORT > $O/ncu_full.log 2>&1
 ncu -i $O/trsv_$R.ncu-rep --page raw --csv > $O/trsv_$R.raw.csv
+rm -f $O/trsv_$R.ncu-rep  # gpurun copies back at most 64 MiB
 fi
 
 if [ "$PART" = all ] || [ "$PART" = c4 ]; then
@@ -37,7 +38,8 @@ $C4 > $O/c4_short.jsonl 2> $O/c4_short.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_config4_n2m_$R.csv $C4 > $O/ncu_c4_launch.log 2>&1
 KT="python scripts/kernel_table.py --n 2000000 --reps 1"
 $KT > $O/kernel_table_config4_n2m_$R.json 2> $O/kt2m.err
-ncu --set full --clock-control none --import-source on -k regex:"k_spmv|k_trsv_wide" -o $O/kt_$R -f $KT > $O/ncu_kt.log 2>&1
+ncu --set full --clock-control none -k regex:"k_spmv|k_trsv_wide" -o $O/kt_$R -f $KT > $O/ncu_kt.log 2>&1
 ncu -i $O/kt_$R.ncu-rep --page raw --csv > $O/kt_$R.raw.csv
+rm -f $O/kt_$R.ncu-rep
 fi
 echo done

@@ -136,7 +136,7 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
         assert check(W2, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levels"
 
 
-@pytest.mark.parametrize("grid", ["lsync", "syncfree"])
+@pytest.mark.parametrize("grid", ["lsync", "syncfree", "syncfree-pipelined", "syncfree-unsorted", "syncfree-n4"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -145,6 +145,12 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     without blocking (a dependency may sit in another lane of the warp)."""
     if grid == "lsync":
         monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
+    if grid == "syncfree-pipelined":
+        monkeypatch.setenv("RSB_WIDE_EARLY", "0")
+    if grid == "syncfree-unsorted":
+        monkeypatch.setenv("RSB_TRSV_SORT", "0")
+    if grid == "syncfree-n4":  # 4 register entries: every longer task takes the batched tail
+        monkeypatch.setenv("RSB_WIDE_N", "4")
     rng = np.random.default_rng(100 + k)
     Ms = leveled_lower([5000] * 4, k, rng, window=4000)  # strictly lower: the unit kinds
     b = rng.standard_normal(Ms.ncols)
@@ -159,7 +165,7 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     U = transpose(M)
     for kind in (L.TRI_UPPER, L.TRI_UPPER_T):
         check(U, kind, b, monkeypatch)
-    assert variant(M, L.TRI_LOWER)[0] == ("grid" if grid == "syncfree" else "lsync")
+    assert variant(M, L.TRI_LOWER)[0] == ("lsync" if grid == "lsync" else "grid")
 
 
 def test_many_chunks_every_kind(monkeypatch):
