@@ -1181,11 +1181,9 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
     } else if (T.lsync) {
         RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
     } else if (T.wide) {
-        k_gather_pos<<<grid_stride(T.n), kBlock, 0, ctx->stream>>>(T.n, T.n, T.task_row, a, c, v.bpos, g);
-        RSB_TRY(post_launch(ctx));
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
-        RSB_TRY(launch_trsv_wide(ctx, T, v, v.bpos, x, g));
+        RSB_TRY(launch_trsv_wide(ctx, T, v, a, c, x, g));
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         // blocks number themselves in start order from this counter

@@ -350,7 +350,7 @@ int get_tri(rsb_mat *T, int kind, TriSched **out);
 int prepare_trsv_cta(int64_t n);
 int prepare_trsv_lean(int64_t smem_bytes);
 int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
-int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g);
+int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g);
 int launch_trsv_lsync(rsb_ctx *ctx, const TriSched &T, const TriDev &v, unsigned *counters, VecIn a,
                       const double *c, double *x, Gate g);
 constexpr size_t kLsCounters = 32 + (size_t)kLsMaxLevels * kLsRep;

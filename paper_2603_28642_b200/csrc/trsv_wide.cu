@@ -4,8 +4,8 @@
 // Persistent warps take 32-task slices in level order from an atomic ticket
 // (a slice only depends on earlier positions, held by running warps or its
 // own lanes, so the order cannot deadlock).  A lane loads its whole task at
-// once -- the right-hand side pre-gathered into position order (one coalesced
-// load, no row -> rhs dependency), its entries (up to N in registers) and the
+// once -- its row and right-hand side (a gather through the row, in flight
+// with the entry loads), its entries (up to N in registers) and the
 // diagonal -- then polls only the operands still missing, all of them per
 // round, through L2 with relaxed gpu-scope loads: a value is published by
 // overwriting the output's sentinel, so a poll that finds it ready is also
@@ -128,169 +128,185 @@ __device__ __noinline__ double wide_tail(const TriDev &T, int64_t base, int lane
     return (MODE & 1) ? __dsub_rn(acc, dot) : acc;
 }
 
-// resident blocks the register budget is sized for: fewer registers per task
-// (smaller N) buy more warps in flight, which is what the solve is bound by
-template <int N>
+// resident blocks the register budget is sized for: fewer registers per lane
+// (smaller N * P) buy more warps in flight
+template <int R>
 struct WideOcc {
-    static constexpr int value = N <= 4 ? 6 : (N <= 8 ? 4 : 3);
+    static constexpr int value = R <= 4 ? 6 : (R <= 8 ? 4 : 3);
 };
 
-template <int MODE, int N, bool TAIL>
-__global__ void __launch_bounds__(kWideBlock, WideOcc<N>::value) k_trsv_wide(TriDev T, const double *bpos, double *x, int nslices,
-                                                          unsigned max_backoff, int EARLY, Gate g) {
+// P consecutive slices per ticket, each lane holding one task of each: the
+// tasks of a ticket are polled together (no slice waits behind another), and
+// the ticket counter -- one address all warps hit -- sees P times fewer
+// atomics.  A task may depend on an earlier task of its own ticket (even its
+// own lane's): the warp-synchronous rounds publish it first.
+template <int MODE, int N, bool TAIL, int P>
+__global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide(TriDev T, VecIn a, const double *c,
+                                                                               double *x, int nslices, unsigned max_backoff,
+                                                                               Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
+    const int ntickets = (nslices + P - 1) / P;
     auto take = [&]() {
         int s = 0;
         if (lane == 0) s = (int)atomicAdd(T.ticket, 1ull);
         return __shfl_sync(0xffffffffu, s, 0);
     };
-    int s = take();
-    if (T.prof && s == 0 && lane == 0) {  // diagnostics: start stamp
+    int j = take();
+    if (T.prof && j == 0 && lane == 0) {  // diagnostics: start stamp
         unsigned long long ts;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts));
         T.prof[7] = (long long)ts;
     }
-    // Optional software pipelining over slices (EARLY): the next slice's
-    // ticket is taken while this slice's task loads are in flight, and its
-    // entry offsets are loaded while this slice polls.  Holding the next
-    // ticket cannot deadlock (it is started after the current slice, whose
-    // dependencies all precede it), but measured slower: the held slice
-    // waits behind the current one instead of being taken by a free warp.
-    int64_t base = 0, base_end = 0;
-    if (s < nslices) {
-        base = T.slice_off[s];
-        base_end = T.slice_off[s + 1];
-    }
-    while (s < nslices) {
-        int nxt_raw = 0;
-        if (EARLY && lane == 0) nxt_raw = (int)atomicAdd(T.ticket, 1ull);
-        const int t = s * 32 + lane;
-        const bool valid = t < T.n;
-        const int K = (int)((base_end - base) >> 5);
-        int row = -1, len = 0;
-        double acc = 0.0, d = 1.0;
-        int cols[N];
-        double vals[N], xv[N];
-        unsigned need = 0;
-        if (valid) {
-            row = T.task_row[t];
-            acc = bpos[t];
-            if (MODE & 2) d = T.diag[t];
+    while (j < ntickets) {
+        int row[P], len[P];
+        double acc[P], d[P];
+        int cols[P][N];
+        double vals[P][N], xv[P][N];
+        unsigned need[P], prev_need[P];
+        bool done[P];
+        int64_t base[P];
+#pragma unroll
+        for (int u = 0; u < P; ++u) {
+            const int s = j * P + u;
+            const int t = s * 32 + lane;
+            const bool valid = s < nslices && t < T.n;
+            row[u] = -1;
+            len[u] = 0;
+            acc[u] = 0.0;
+            d[u] = 1.0;
+            need[u] = 0;
+            prev_need[u] = ~0u;
+            base[u] = 0;
+            int K = 0;
+            if (s < nslices) {
+                base[u] = T.slice_off[s];
+                K = (int)((T.slice_off[s + 1] - base[u]) >> 5);
+            }
 #pragma unroll
             for (int q = 0; q < N; ++q) {
-                cols[q] = -1;
-                vals[q] = 0.0;
-                xv[q] = 0.0;
-                if (q < K) {
-                    cols[q] = T.ecol[base + (int64_t)q * 32 + lane];
-                    vals[q] = T.eval[base + (int64_t)q * 32 + lane];
-                }
+                cols[u][q] = -1;
+                vals[u][q] = 0.0;
+                xv[u][q] = 0.0;
             }
+            if (valid) {
+                // the right-hand side a(row) [+ c[row]] is read here (the
+                // permutation gather fused): its load overlaps the entry loads
+                row[u] = T.task_row[t];
+                acc[u] = a.g ? a.p[a.g[row[u] + a.off]] : a.p[row[u] + a.off];
+                if (c) acc[u] = __dadd_rn(acc[u], c[row[u]]);
+                if (MODE & 2) d[u] = T.diag[t];
 #pragma unroll
-            for (int q = 0; q < N; ++q)
-                if (cols[q] >= 0) {
-                    need |= 1u << q;
-                    ++len;
-                }
-            if (TAIL && len == N && K > N)  // entries continue past the registers
-                len = wide_tail_len(T, base, lane, N, K);
-        }
-        int nxt = 0;
-        int64_t nbase = 0, nbase_end = 0;
-        if (EARLY) {
-            nxt = __shfl_sync(0xffffffffu, nxt_raw, 0);
-            if (nxt < nslices) {
-                nbase = T.slice_off[nxt];
-                nbase_end = T.slice_off[nxt + 1];
+                for (int q = 0; q < N; ++q)
+                    if (q < K) {
+                        cols[u][q] = T.ecol[base[u] + (int64_t)q * 32 + lane];
+                        vals[u][q] = T.eval[base[u] + (int64_t)q * 32 + lane];
+                    }
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (cols[u][q] >= 0) {
+                        need[u] |= 1u << q;
+                        ++len[u];
+                    }
+                if (TAIL && len[u] == N && K > N)  // entries continue past the registers
+                    len[u] = wide_tail_len(T, base[u], lane, N, K);
             }
+            done[u] = !valid;
         }
-        bool done = !valid;
-        // warp-synchronous polling: every round each pending lane loads all
-        // of its missing operands; the ready lanes compute and publish.  A
+        // warp-synchronous polling: every round each pending task loads all
+        // of its missing operands; the ready ones compute and publish.  A
         // round without progress backs off, so that thousands of waiting warps
         // do not flood L2 with polls while the frontier level is computed.
-        unsigned backoff = 0, prev_need = ~0u;
-        while (__any_sync(0xffffffffu, !done)) {
-            if (__all_sync(0xffffffffu, done || need == prev_need) && backoff) __nanosleep(backoff);
-            prev_need = need;
+        unsigned backoff = 0;
+        for (;;) {
+            bool pending = false, stalled = true;
+#pragma unroll
+            for (int u = 0; u < P; ++u) {
+                pending |= !done[u];
+                stalled &= done[u] || need[u] == prev_need[u];
+            }
+            if (!__any_sync(0xffffffffu, pending)) break;
+            if (__all_sync(0xffffffffu, stalled) && backoff) __nanosleep(backoff);
             backoff = backoff ? min(backoff * 2, max_backoff) : kWideMinBackoffNs;
-            if (!done) {
+#pragma unroll
+            for (int u = 0; u < P; ++u) {
+                prev_need[u] = need[u];
+                if (done[u]) continue;
                 unsigned long long pv[N];
 #pragma unroll
                 for (int q = 0; q < N; ++q) {
                     pv[q] = kSentinel;
-                    poll_if((need >> q) & 1u, x + (cols[q] >= 0 ? cols[q] : 0), pv[q]);
+                    poll_if((need[u] >> q) & 1u, x + (cols[u][q] >= 0 ? cols[u][q] : 0), pv[q]);
                 }
 #pragma unroll
                 for (int q = 0; q < N; ++q)
-                    if (((need >> q) & 1u) && pv[q] != kSentinel) {
-                        xv[q] = __longlong_as_double((long long)pv[q]);
-                        need &= ~(1u << q);
+                    if (((need[u] >> q) & 1u) && pv[q] != kSentinel) {
+                        xv[u][q] = __longlong_as_double((long long)pv[q]);
+                        need[u] &= ~(1u << q);
                     }
-                if (need == 0 && (!TAIL || len <= N || wide_tail_ready(T, base, lane, N, len, x))) {
-                    double r = acc;
+                if (need[u] == 0 && (!TAIL || len[u] <= N || wide_tail_ready(T, base[u], lane, N, len[u], x))) {
+                    double r = acc[u];
                     if (!(MODE & 1)) {
 #pragma unroll
                         for (int q = 0; q < N; ++q)
-                            if (q < len && xv[q] != 0.0) r = __dsub_rn(r, __dmul_rn(vals[q], xv[q]));
-                        if (TAIL && len > N) r = wide_tail<MODE>(T, base, lane, N, len, r, 0.0, x);
-                    } else if (len > 0) {  // < 16 entries (the scalar OpenBLAS order; checked at analysis)
+                            if (q < len[u] && xv[u][q] != 0.0) r = __dsub_rn(r, __dmul_rn(vals[u][q], xv[u][q]));
+                        if (TAIL && len[u] > N) r = wide_tail<MODE>(T, base[u], lane, N, len[u], r, 0.0, x);
+                    } else if (len[u] > 0) {  // < 16 entries (the scalar OpenBLAS order; checked at analysis)
                         double dot = 0.0;
 #pragma unroll
                         for (int q = 0; q < N; ++q)
-                            if (q < len) dot = fma(vals[q], xv[q], dot);
-                        r = (TAIL && len > N) ? wide_tail<MODE>(T, base, lane, N, len, r, dot, x) : __dsub_rn(r, dot);
+                            if (q < len[u]) dot = fma(vals[u][q], xv[u][q], dot);
+                        r = (TAIL && len[u] > N) ? wide_tail<MODE>(T, base[u], lane, N, len[u], r, dot, x)
+                                                 : __dsub_rn(r, dot);
                     }
-                    if (MODE & 2) r = __ddiv_rn(r, d);
-                    if (row >= 0) st_relaxed_f64(x + row, r);
-                    done = true;
+                    if (MODE & 2) r = __ddiv_rn(r, d[u]);
+                    if (row[u] >= 0) st_relaxed_f64(x + row[u], r);
+                    done[u] = true;
                 }
             }
             __syncwarp();
         }
-        if (EARLY) {
-            s = nxt;
-            base = nbase;
-            base_end = nbase_end;
-        } else {
-            s = take();
-            if (s < nslices) {
-                base = T.slice_off[s];
-                base_end = T.slice_off[s + 1];
-            }
-        }
+        j = take();
     }
 }
 
-using WideKernel = void (*)(TriDev, const double *, double *, int, unsigned, int, Gate);
+using WideKernel = void (*)(TriDev, VecIn, const double *, double *, int, unsigned, Gate);
 
-template <int MODE>
+template <int MODE, int P>
 WideKernel wide_kernel(int n, bool tail) {
-    if (n <= 4) return tail ? k_trsv_wide<MODE, 4, true> : k_trsv_wide<MODE, 4, false>;
-    if (n <= 8) return tail ? k_trsv_wide<MODE, 8, true> : k_trsv_wide<MODE, 8, false>;
-    return tail ? k_trsv_wide<MODE, 12, true> : k_trsv_wide<MODE, 12, false>;
+    if (n <= 4) return tail ? k_trsv_wide<MODE, 4, true, P> : k_trsv_wide<MODE, 4, false, P>;
+    if (n <= 8) return tail ? k_trsv_wide<MODE, 8, true, P> : k_trsv_wide<MODE, 8, false, P>;
+    return tail ? k_trsv_wide<MODE, 12, true, P> : k_trsv_wide<MODE, 12, false, P>;
 }
 
-WideKernel wide_kernel_for(int mode, int n, bool tail) {
+WideKernel wide_kernel_for(int mode, int n, bool tail, int p) {
+    if (p == 2) switch (mode) {
+            case 0: return wide_kernel<0, 2>(n, tail);
+            case 1: return wide_kernel<1, 2>(n, tail);
+            case 2: return wide_kernel<2, 2>(n, tail);
+            default: return wide_kernel<3, 2>(n, tail);
+        }
     switch (mode) {
-        case 0: return wide_kernel<0>(n, tail);
-        case 1: return wide_kernel<1>(n, tail);
-        case 2: return wide_kernel<2>(n, tail);
-        default: return wide_kernel<3>(n, tail);
+        case 0: return wide_kernel<0, 1>(n, tail);
+        case 1: return wide_kernel<1, 1>(n, tail);
+        case 2: return wide_kernel<2, 1>(n, tail);
+        default: return wide_kernel<3, 1>(n, tail);
     }
 }
 
 }  // namespace
 
-int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const double *bpos, double *x, Gate g) {
+int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g) {
     // registers hold wide_n entries per task (most tasks fit);
-    // longer tasks take the batched out-of-line tail
+    // longer tasks take the batched out-of-line tail.  RSB_WIDE_P: slices per
+    // ticket (experiments)
     const bool tail = T.max_task > T.wide_n;
-    WideKernel k = wide_kernel_for(T.mode, T.wide_n, tail);
-    static int per_sm[4][3][2] = {};  // occupancy of each instantiation, queried once
+    const char *ep = getenv("RSB_WIDE_P");
+    const int p = (ep && atoi(ep) == 2) ? 2 : 1;
+    WideKernel k = wide_kernel_for(T.mode, T.wide_n, tail, p);
+    static int per_sm[4][3][2][2] = {};  // occupancy of each instantiation, queried once
     const int ni = T.wide_n <= 4 ? 0 : (T.wide_n <= 8 ? 1 : 2);
-    int &occ = per_sm[T.mode & 3][ni][tail ? 1 : 0];
+    int &occ = per_sm[T.mode & 3][ni][tail ? 1 : 0][p - 1];
     if (occ == 0) {
         RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWideBlock, 0));
         occ = std::max(occ, 1);
@@ -303,13 +319,8 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, const dou
     const char *eo = getenv("RSB_WIDE_OCC"), *eb = getenv("RSB_WIDE_BACKOFF");
     const int use_occ = eo ? std::max(1, std::min(occ, atoi(eo))) : occ;
     const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
-    const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ, (nslices * 32 + kWideBlock - 1) / kWideBlock);
-    // RSB_WIDE_EARLY=1: software pipelining over slices (experiments; measured
-    // slower on config 4 at n = 2e6: U 0.45 vs 0.30 ms -- a warp holding its
-    // next slice delays that slice behind its current one)
-    const char *ee = getenv("RSB_WIDE_EARLY");
-    const int early = (ee && atoi(ee) == 1) ? 1 : 0;
-    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, bpos, x, nslices, max_backoff, early, g);
+    const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ, ((int64_t)nslices * 32 / p + kWideBlock - 1) / kWideBlock);
+    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, a, c, x, nslices, max_backoff, g);
     return RSB_OK;
 }
 

@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 DEFAULT_SETS = ["default=", "nosort=RSB_TRSV_SORT=0", "n12=RSB_WIDE_N=12", "n8=RSB_WIDE_N=8",
                 "lsync=RSB_TRSV_GRID=lsync"]
-KNOBS = ("RSB_TRSV_SORT", "RSB_WIDE_N", "RSB_TRSV_GRID", "RSB_WIDE_OCC", "RSB_WIDE_BACKOFF", "RSB_WIDE_EARLY")
+KNOBS = ("RSB_TRSV_SORT", "RSB_WIDE_N", "RSB_TRSV_GRID", "RSB_WIDE_OCC", "RSB_WIDE_BACKOFF", "RSB_WIDE_P")
 
 
 def main():

@@ -136,7 +136,7 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
         assert check(W2, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levels"
 
 
-@pytest.mark.parametrize("grid", ["lsync", "syncfree", "syncfree-pipelined", "syncfree-unsorted", "syncfree-n4"])
+@pytest.mark.parametrize("grid", ["lsync", "syncfree", "syncfree-pairs", "syncfree-unsorted", "syncfree-n4"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -145,7 +145,7 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     without blocking (a dependency may sit in another lane of the warp)."""
     if grid == "lsync":
         monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
-    if grid == "syncfree-pipelined":
+    if grid == "syncfree-pairs":
         monkeypatch.setenv("RSB_WIDE_EARLY", "0")
     if grid == "syncfree-unsorted":
         monkeypatch.setenv("RSB_TRSV_SORT", "0")
