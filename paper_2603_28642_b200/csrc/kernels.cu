@@ -1181,9 +1181,9 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
     } else if (T.lsync) {
         RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
     } else if (T.wide) {
-        RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
-        RSB_TRY(launch_trsv_wide(ctx, T, v, a, c, x, g));
+        RSB_TRY(launch_trsv_wide(ctx, T, v, a, c, x, g));  // prologue (level 0 + sentinel fill), then the solve
+        ctx->launches += 1;
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         // blocks number themselves in start order from this counter

@@ -142,11 +142,12 @@ struct WideOcc {
 // own lane's): the warp-synchronous rounds publish it first.
 template <int MODE, int N, bool TAIL, int P>
 __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide(TriDev T, VecIn a, const double *c,
-                                                                               double *x, int nslices, unsigned max_backoff,
-                                                                               Gate g) {
+                                                                               double *x, int first_slice, int nslices,
+                                                                               unsigned max_backoff, Gate g) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
-    const int ntickets = (nslices + P - 1) / P;
+    // slices wholly inside level 0 were solved by the prologue
+    const int ntickets = (nslices - first_slice + P - 1) / P;
     auto take = [&]() {
         int s = 0;
         if (lane == 0) s = (int)atomicAdd(T.ticket, 1ull);
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide
         int64_t base[P];
 #pragma unroll
         for (int u = 0; u < P; ++u) {
-            const int s = j * P + u;
+            const int s = first_slice + j * P + u;
             const int t = s * 32 + lane;
             const bool valid = s < nslices && t < T.n;
             row[u] = -1;
@@ -270,7 +271,30 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide
     }
 }
 
-using WideKernel = void (*)(TriDev, VecIn, const double *, double *, int, unsigned, Gate);
+// Prologue of a wide solve, one pass over the positions: level-0 tasks have
+// no dependencies, so they are solved here (x = rhs, divided by the diagonal
+// for the non-unit kinds -- the same operations as the main kernel), and
+// every other unknown is set to the sentinel the main kernel polls.  The main
+// kernel then skips the slices that lie wholly in level 0 (on config 4 at
+// mu = 1 a quarter of L1's unknowns).
+template <int MODE>
+__global__ void k_wide_prologue(TriDev T, VecIn a, const double *c, double *x, int32_t lvl1, Gate g) {
+    if (gated(g)) return;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T.n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int row = T.task_row[t];
+        unsigned long long bits = kSentinel;
+        if (t < lvl1) {
+            double r = a.g ? a.p[a.g[row + a.off]] : a.p[row + a.off];
+            if (c) r = __dadd_rn(r, c[row]);
+            if (MODE & 2) r = __ddiv_rn(r, T.diag[t]);
+            bits = __double_as_longlong(r);
+            if (bits == kSentinel) bits = 0x7FF8000000000000ull;
+        }
+        reinterpret_cast<unsigned long long *>(x)[row] = bits;
+    }
+}
+
+using WideKernel = void (*)(TriDev, VecIn, const double *, double *, int, int, unsigned, Gate);
 
 template <int MODE, int P>
 WideKernel wide_kernel(int n, bool tail) {
@@ -314,13 +338,26 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, 
     int sms = 0;
     RSB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
     const int nslices = (T.n + 31) / 32;
+    const int32_t lvl1 = T.h_level_ptr.size() > 1 ? T.h_level_ptr[1] : T.n;  // level-0 positions
+    const int first_slice = lvl1 / 32;
+    {
+        const int pg = (int)std::min<int64_t>(((int64_t)T.n + 255) / 256, (int64_t)sms * 8);
+        switch (T.mode & 3) {
+            case 0: k_wide_prologue<0><<<pg, 256, 0, ctx->stream>>>(v, a, c, x, lvl1, g); break;
+            case 1: k_wide_prologue<1><<<pg, 256, 0, ctx->stream>>>(v, a, c, x, lvl1, g); break;
+            case 2: k_wide_prologue<2><<<pg, 256, 0, ctx->stream>>>(v, a, c, x, lvl1, g); break;
+            default: k_wide_prologue<3><<<pg, 256, 0, ctx->stream>>>(v, a, c, x, lvl1, g); break;
+        }
+        RSB_TRY_CUDA(cudaGetLastError());
+    }
     // experiments: RSB_WIDE_OCC caps the resident blocks per SM, RSB_WIDE_BACKOFF
     // sets the longest back-off (ns) of a waiting warp
     const char *eo = getenv("RSB_WIDE_OCC"), *eb = getenv("RSB_WIDE_BACKOFF");
     const int use_occ = eo ? std::max(1, std::min(occ, atoi(eo))) : occ;
     const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
-    const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ, ((int64_t)nslices * 32 / p + kWideBlock - 1) / kWideBlock);
-    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, a, c, x, nslices, max_backoff, g);
+    const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ,
+                                            ((int64_t)(nslices - first_slice) * 32 / p + kWideBlock - 1) / kWideBlock);
+    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, a, c, x, first_slice, nslices, max_backoff, g);
     return RSB_OK;
 }
 
