@@ -1,5 +1,5 @@
 #!/bin/bash
-O=gpurun_out/r01n
+O=gpurun_out/r01o
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo pytest=$? >> $O/pytest_gpu.log
 tail -3 $O/pytest_gpu.log
