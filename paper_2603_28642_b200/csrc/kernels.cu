@@ -712,6 +712,9 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
 // right-hand side in task-position order: bpos[t] = a(row_t) [+ c[row_t]]
 __global__ void k_gather_pos(int32_t n, int64_t padded, const int32_t *task_row, VecIn a, const double *c,
                              double *bpos, Gate g) {
+    // let the solve that consumes bpos start its prologue (it waits for this
+    // grid's completion before reading anything written here)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (gated(g)) return;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < padded; t += (int64_t)gridDim.x * blockDim.x) {
         double v = 0.0;

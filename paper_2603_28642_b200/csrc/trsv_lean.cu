@@ -169,7 +169,10 @@ __device__ __forceinline__ double2 lds_v2f64(unsigned a) {
 }
 template <int MODE, int N>
 __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x, Gate g) {
-    if (gated(g)) return;
+    // Launched as a programmatic dependent of k_gather_pos: everything up to
+    // griddepcontrol.wait below touches only the schedule (static since the
+    // analysis) and shared memory, so it overlaps the gather; the gate, the
+    // gathered right-hand side and x are touched only after the wait.
     constexpr bool kDiag = (MODE & 2) != 0;
     constexpr int NS = 4 * ((N + 3) / 4), NQ = NS / 4, NP = NS / 2;
     __shared__ __align__(16) double ring[kRing + 2];  // values by task position; ring[kRing] = 0
@@ -184,16 +187,46 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     int *lvl = reinterpret_cast<int *>(full + 2 * kStageBufs);
     const int nlev = T.nlevels;
     int2 *ev = reinterpret_cast<int2 *>(lvl + ((nlev + 8) & ~3));
-    // level bounds, padded with the end so lvl[l + 3] is always valid
-    for (int i = threadIdx.x; i <= nlev + 4; i += blockDim.x) lvl[i] = T.level_ptr[i < nlev ? i : nlev];
+    const long long t_entry = T.prof ? clock64() : 0;
+    // level bounds, padded with the end so lvl[l + 3] is always valid, and the
+    // producer's event list: kPro loads in flight per thread before any store
+    // (one global round trip per kPro * blockDim entries, not per blockDim --
+    // U on config 1 has 2,806 levels)
+    {
+        constexpr int kPro = 8;
+        const int nl = nlev + 5, ne = T.lean_nev, stride = (int)blockDim.x;
+        for (int i0 = threadIdx.x; i0 < nl; i0 += kPro * stride) {
+            int v[kPro];
+#pragma unroll
+            for (int u = 0; u < kPro; ++u) {
+                const int i = i0 + u * stride;
+                v[u] = i < nl ? __ldg(T.level_ptr + (i < nlev ? i : nlev)) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kPro; ++u)
+                if (i0 + u * stride < nl) lvl[i0 + u * stride] = v[u];
+        }
+        for (int i0 = threadIdx.x; i0 < ne; i0 += kPro * stride) {
+            int2 v[kPro];
+#pragma unroll
+            for (int u = 0; u < kPro; ++u) {
+                const int i = i0 + u * stride;
+                v[u] = i < ne ? __ldg(T.lean_ev + i) : make_int2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kPro; ++u)
+                if (i0 + u * stride < ne) ev[i0 + u * stride] = v[u];
+        }
+    }
     for (int i = threadIdx.x; i < NS * 32; i += blockDim.x) zsrc[i] = kRing * 8;
-    for (int i = threadIdx.x; i < T.lean_nev; i += blockDim.x) ev[i] = T.lean_ev[i];
     if (threadIdx.x == 0) {
         ring[kRing] = 0.0;
         for (int b = 0; b < kStageBufs; ++b) mbar_init(&full[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // k_gather_pos (and all before it) complete
+    if (gated(g)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = (int)(blockDim.x >> 5) - 1;  // consumer warps
     const int pwarp = nwarps == 4 ? 3 : nwarps;      // producer warp
@@ -340,6 +373,7 @@ __global__ void __launch_bounds__(kLeanThreads) k_trsv_lean(TriDev T, double *x,
     }
     if (l < nlev) level(l, A, Bt);  // the last level when nlev is odd
     if (prof) {
+        T.prof[7] = tp - t_entry;  // prologue: entry to the first level
         T.prof[0] = 0;
         T.prof[1] = clock64() - tp;
         T.prof[2] = 1;
@@ -408,7 +442,19 @@ int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x
     const size_t smem =
         (size_t)lean_dyn_smem_bytes(T.stage_ch, (T.lean_n + 3) & ~3, T.diag != nullptr, T.nlevels, T.nchunks);
     const int warps = (int)std::min<int64_t>(4, std::max<int64_t>(1, (T.max_width + 31) / 32));
-    k<<<1, 32 * (warps + 1), smem, ctx->stream>>>(v, x, g);
+    // programmatic dependent launch: the prologue runs while k_gather_pos
+    // (which triggers its dependents on entry) is still working
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32 * (warps + 1));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, v, x, g));
     return RSB_OK;
 }
 

@@ -23,5 +23,6 @@ for name, M, kind in (("L1", f.L1, L.TRI_LOWER_UNIT), ("L1T", f.L1, L.TRI_LOWER_
     L.check(L.lib().rsb_trsv_profile(dm.h, kind, c))
     nl, ns = c[5], max(c[2], 1)
     out[name] = {"cycles_per_level": round(c[1] / nl, 1), 
-                 "producer_chunk_wait_per_level": round(c[6] / nl, 1), "levels": nl, "chunks": c[4]}
+                 "producer_chunk_wait_per_level": round(c[6] / nl, 1),
+                 "prologue_cycles": c[7], "loop_cycles": c[1], "levels": nl, "chunks": c[4]}
 print(json.dumps(out))
