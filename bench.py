@@ -231,6 +231,9 @@ def ncu_traffic():
 # ---------------------------------------------------------------------------
 
 
+CPU_THREADS_NOTE = ("one core: the reference solve is sequential (triangular solves, np.add.at / reduceat scatters in numpy); only its BLAS dots could use more threads, and the port runs them in the reference's one-thread OpenBLAS order (--blas-threads T selects the T-thread order)")
+
+
 def cpu_oracle_rate(S, pre, b, norm_a, budget_s, max_iters_cap=400):
     """Oracle port of pcgls (oracle/oracle.py), single thread, fixed-iteration
     run sized to roughly budget_s seconds; returns (iters/s, iters, seconds)."""
@@ -275,7 +278,8 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic (seeded generators, workloads.py)",
         "config": {"workload": name, "mu": args.mu, "coupling": mode, "p": st["p"], "tau": st["tau"]},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port",
-                         "sample": f"{k} fixed iterations (delta=1e-300) of the oracle port of pcgls"},
+                         "sample": f"{k} fixed iterations (delta=1e-300) of the oracle port of pcgls",
+                         "threads": CPU_THREADS_NOTE},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -405,7 +409,8 @@ def run_b200(args):
         rate, kc, dtc = cpu_oracle_rate(S, pre, b, norm_a, args.cpu_seconds)
         cpu = {"value": rate, "unit": "iter/s", "cores": 1, "kind": "port",
                "sample": f"{kc} fixed iterations (delta=1e-300) of the oracle port of pcgls on the same "
-                         f"workload, {dtc:.1f} s, host has {os.cpu_count()} cores"}
+                         f"workload, {dtc:.1f} s, host has {os.cpu_count()} cores",
+               "threads": CPU_THREADS_NOTE}
     line = {
         "metric": "preconditioned CGLS iterations/s",
         "value": value,
