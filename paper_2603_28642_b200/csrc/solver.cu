@@ -327,6 +327,11 @@ int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
         k_cg_alpha<<<1, 1, 0, ctx->stream>>>(cg, g);
         RSB_TRY(chk(ctx));
         RSB_TRY(launch_axpy(ctx, W.w, W.cg_p, &cg->alpha, +1, s, g));
+        // the last step's r, rho_new, break test and p feed nothing: w is final
+        // here and the next application starts from k_cg_init / k_cg_start
+        // (which resets the stop flag), so they are not enqueued -- w, and so
+        // every apply, is unchanged bit for bit
+        if (it + 1 == P->cg_iters) break;
         RSB_TRY(launch_axpy(ctx, W.cg_r, W.cg_q, &cg->alpha, -1, s, g));
         RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_r, nullptr, 0}, VecIn{W.cg_r, nullptr, 0}, &cg->rho_new, 0, g, nullptr));
         k_cg_beta<<<1, 1, 0, ctx->stream>>>(cg, g);
