@@ -132,3 +132,28 @@ def test_s_matvec_zero_l2_and_hand_case():
                                                csc([[2.0, 0.0]]), P.CscMatrix.identity(2), 0,
                                                np.zeros(3, dtype=np.int64)), s_mode=P.SMode.DENSE_FACTOR)
     assert np.array_equal(pre.y_apply([3.0, 5.0]), [6.0])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 5])
+def test_inner_cg_step_counts_bitwise(k):
+    """_cg_fixed_steps (pc.py:284-310) with k steps: the device skips the last
+    step's r / rho_new / p updates (they feed nothing), so w and the apply must
+    still equal the oracle bit for bit -- also on applications that follow an
+    early break (rho = 0 on a zero u), which must not leak their stop flag."""
+    from paper_2603_28642_b200 import workloads as W
+
+    A, _ = W.config0(seed=7, m=600, n=400)
+    S, _ = P.column_scale(A)
+    f = P.ilup_factorize(S, P.IlupParams(p=10, tau=1e-3, mu=1.0))
+    pre = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG, cg_iters=k)
+    op = O.OraclePreconditioner.from_reference(pre)
+    rng = np.random.default_rng(k)
+    r1, r2 = rng.standard_normal(400), rng.standard_normal(200)
+    assert np.array_equal(pre.apply(r1, r2), op.apply(r1, r2))
+    assert np.array_equal(pre.s_matvec_implicit(r2), op.s_matvec_implicit(r2))
+    # r2 = Y r1 makes u = 0: the inner CG stops at rho == 0 (w = 0)
+    u0 = pre.y_apply(r1)
+    assert np.array_equal(pre.apply(r1, u0), op.apply(r1, u0))
+    # and the next application runs all k steps again
+    r1b, r2b = rng.standard_normal(400), rng.standard_normal(200)
+    assert np.array_equal(pre.apply(r1b, r2b), op.apply(r1b, r2b))
