@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "rsb_internal.h"
@@ -1030,31 +1031,45 @@ int rsb_pcgls_many(int count, rsb_solver *const *S, const double *const *b, int 
                 set_error("rsb_pcgls_many needs distinct solvers on distinct contexts");
                 return RSB_EINVAL;
             }
+    // How many solves iterate at once.  Single-CTA triangular solves (narrow
+    // DAGs) occupy one SM each, so all run together; a grid-wide solve fills
+    // the GPU on its own and concurrent ones only contend (config 4 at n = 8e6:
+    // 8 concurrent RHS 74 RHS-iterations/s against 95 for one), so those run
+    // one after another.  RSB_BATCH_CONC overrides (experiments).
+    int conc = count;
+    for (int i = 0; i < count; ++i)
+        if (S[i]->pre)
+            for (const TriSched *T : {S[i]->pre->tL1, S[i]->pre->tL1T, S[i]->pre->tU})
+                if (T && !T->single_cta) conc = 1;
+    if (const char *e = getenv("RSB_BATCH_CONC")) conc = std::max(1, atoi(e));
     std::vector<int> st(count, ST_RUN);
     for (int i = 0; i < count; ++i) RSB_TRY(start_enqueue(S[i], b[i], where, cfg));
     for (int i = 0; i < count; ++i) RSB_TRY(start_complete(S[i], &st[i]));
     std::vector<int64_t> done(count, 0);
-    int64_t batch = 4;
-    for (;;) {
-        bool any = false;
-        for (int i = 0; i < count; ++i) {
-            if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
-            RSB_TRY(iterate_enqueue(S[i], std::min(batch, cfg->max_iters - done[i])));
-            any = true;
-        }
-        if (!any) break;
-        for (int i = 0; i < count; ++i) {
-            if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
-            done[i] += std::min(batch, cfg->max_iters - done[i]);
-            RSB_TRY_CUDA(cudaSetDevice(S[i]->ctx->device));
-            RSB_TRY_CUDA(cudaStreamSynchronize(S[i]->ctx->stream));
-            st[i] = S[i]->h_st->status;
-            if (st[i] == ST_ERROR) {
-                set_error("zero denominator in stopping ratio");
-                return RSB_EINVAL;
+    for (int g0 = 0; g0 < count; g0 += conc) {
+        const int g1 = std::min(count, g0 + conc);
+        int64_t batch = 4;
+        for (;;) {
+            bool any = false;
+            for (int i = g0; i < g1; ++i) {
+                if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
+                RSB_TRY(iterate_enqueue(S[i], std::min(batch, cfg->max_iters - done[i])));
+                any = true;
             }
+            if (!any) break;
+            for (int i = g0; i < g1; ++i) {
+                if (st[i] != ST_RUN || done[i] >= cfg->max_iters) continue;
+                done[i] += std::min(batch, cfg->max_iters - done[i]);
+                RSB_TRY_CUDA(cudaSetDevice(S[i]->ctx->device));
+                RSB_TRY_CUDA(cudaStreamSynchronize(S[i]->ctx->stream));
+                st[i] = S[i]->h_st->status;
+                if (st[i] == ST_ERROR) {
+                    set_error("zero denominator in stopping ratio");
+                    return RSB_EINVAL;
+                }
+            }
+            batch = std::min<int64_t>(batch * 2, 64);
         }
-        batch = std::min<int64_t>(batch * 2, 64);
     }
     for (int i = 0; i < count; ++i) {
         RSB_TRY(rsb_solver_finish(S[i], &reps[i], history ? history + i * history_cap : nullptr,

@@ -163,9 +163,12 @@ def pcgls_batch(A, B, pre, cfg: CglsConfig, streams: int | None = None):
 
     Not in the reference API: the reference solves one b per pcgls call; the
     result for each row of B is exactly pcgls(A, B[j], pre, cfg), bit for
-    bit.  The solves run concurrently, `streams` at a time (default: all),
-    each on its own CUDA stream with its own workspace, reading the one
-    device copy of A and the factors.  Returns (X with rows x_j, [reports]).
+    bit.  Each solve has its own CUDA stream and workspace, `streams` of them
+    per library call (default: all), reading the one device copy of A and the
+    factors.  Inside a call the library iterates them all at once when the
+    triangular solves are single-CTA (narrow DAGs, one SM each) and one after
+    another when they are grid-wide (each fills the GPU; RSB_BATCH_CONC
+    overrides).  Returns (X with rows x_j, [reports]).
     """
     B = np.ascontiguousarray(np.atleast_2d(np.asarray(B, dtype=np.float64)))
     m, n = int(A.nrows), int(A.ncols)
