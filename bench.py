@@ -380,8 +380,8 @@ def run_b200(args):
                  "seconds": b_s,
                  "call": f"pcgls_batch(A, B[{args.batch} x m] host, pre, CglsConfig(delta=1e-300, "
                          f"max_iters={K})): one stream + workspace per RHS, shared A and factors; all RHS "
-                         f"iterate concurrently when the solves are single-CTA, one after another when "
-                         f"they are grid-wide (each fills the GPU)"}
+                         f"iterate concurrently when the solves are single-CTA, two at a time when "
+                         f"they are grid-wide (each fills most of the GPU)"}
 
     # ---- time to tolerance (config delta), device path, reported alongside
     tol = None

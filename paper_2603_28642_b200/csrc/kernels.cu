@@ -1185,8 +1185,8 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
     } else if (T.wide) {
         RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
-        RSB_TRY(launch_trsv_wide(ctx, T, v, a, c, x, g));  // prologue (level 0 + sentinel fill), then the solve
-        ctx->launches += 1;
+        RSB_TRY(launch_trsv_wide(ctx, T, v, a, c, x, g));  // sentinel fill, level 0, then the solve
+        ctx->launches += 1;  // level 0 (the fill counted itself; the solve is counted below)
     } else {
         RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
         // blocks number themselves in start order from this counter

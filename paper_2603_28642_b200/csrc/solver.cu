@@ -1033,14 +1033,16 @@ int rsb_pcgls_many(int count, rsb_solver *const *S, const double *const *b, int 
             }
     // How many solves iterate at once.  Single-CTA triangular solves (narrow
     // DAGs) occupy one SM each, so all run together; a grid-wide solve fills
-    // the GPU on its own and concurrent ones only contend (config 4 at n = 8e6:
-    // 8 concurrent RHS 74 RHS-iterations/s against 95 for one), so those run
-    // one after another.  RSB_BATCH_CONC overrides (experiments).
+    // most of the GPU on its own and many concurrent ones only contend (config
+    // 4 at n = 8e6: 8 concurrent RHS 72 RHS-iterations/s against 84 for one
+    // e2e), while two overlap each other's level tails (n = 2e6: 340 at two,
+    // 290 at one, 325 at 4 or 8; profiles/batch_conc_*), so those run two at a
+    // time.  RSB_BATCH_CONC overrides (experiments).
     int conc = count;
     for (int i = 0; i < count; ++i)
         if (S[i]->pre)
             for (const TriSched *T : {S[i]->pre->tL1, S[i]->pre->tL1T, S[i]->pre->tU})
-                if (T && !T->single_cta) conc = 1;
+                if (T && !T->single_cta) conc = std::min(conc, 2);
     if (const char *e = getenv("RSB_BATCH_CONC")) conc = std::max(1, atoi(e));
     std::vector<int> st(count, ST_RUN);
     for (int i = 0; i < count; ++i) RSB_TRY(start_enqueue(S[i], b[i], where, cfg));

@@ -167,8 +167,8 @@ def pcgls_batch(A, B, pre, cfg: CglsConfig, streams: int | None = None):
     per library call (default: all), reading the one device copy of A and the
     factors.  Inside a call the library iterates them all at once when the
     triangular solves are single-CTA (narrow DAGs, one SM each) and one after
-    another when they are grid-wide (each fills the GPU; RSB_BATCH_CONC
-    overrides).  Returns (X with rows x_j, [reports]).
+    two at a time when they are grid-wide (each fills most of the GPU;
+    RSB_BATCH_CONC overrides).  Returns (X with rows x_j, [reports]).
     """
     B = np.ascontiguousarray(np.atleast_2d(np.asarray(B, dtype=np.float64)))
     m, n = int(A.nrows), int(A.ncols)
