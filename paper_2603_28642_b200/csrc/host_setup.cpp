@@ -59,7 +59,12 @@ double pairwise(const double *a, int64_t n) {
 
 // _dual_drop (il.py:159-167): keep |v| >= tau and v != 0; if more than p
 // remain keep the p largest |v| (ties: smaller id first); return sorted by id.
-void dual_drop(std::vector<int64_t> &ids, std::vector<double> &vals, int64_t p, double tau) {
+// The same rule without sorting the whole column: the p survivors are kept
+// in a small array ordered best-first by (|v| descending, id ascending) --
+// np.lexsort((ids, -abs(vals))) -- while the entries stream past, then put
+// in id order.  ids are unique, so the selection is the same set.
+void dual_drop_fast(std::vector<int64_t> &ids, std::vector<double> &vals, int64_t p, double tau,
+                    std::vector<int64_t> &sid, std::vector<double> &sv) {
     size_t k = 0;
     for (size_t i = 0; i < ids.size(); ++i)
         if (std::fabs(vals[i]) >= tau && vals[i] != 0.0) {
@@ -69,26 +74,71 @@ void dual_drop(std::vector<int64_t> &ids, std::vector<double> &vals, int64_t p, 
         }
     ids.resize(k);
     vals.resize(k);
-    std::vector<size_t> ord(k);
-    std::iota(ord.begin(), ord.end(), 0);
-    if ((int64_t)k > p) {
-        // np.lexsort((ids, -abs(vals))): primary -|v| ascending, secondary id
-        std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-            const double na = -std::fabs(vals[a]), nb = -std::fabs(vals[b]);
-            if (na != nb) return na < nb;
-            return ids[a] < ids[b];
-        });
-        ord.resize(p);
+    auto by_id = [&](std::vector<int64_t> &I, std::vector<double> &V) {
+        for (size_t a = 1; a < I.size(); ++a) {
+            const int64_t ki = I[a];
+            const double kv = V[a];
+            size_t b = a;
+            for (; b > 0 && I[b - 1] > ki; --b) {
+                I[b] = I[b - 1];
+                V[b] = V[b - 1];
+            }
+            I[b] = ki;
+            V[b] = kv;
+        }
+    };
+    if ((int64_t)k <= p) {
+        if (k > 64) {
+            std::vector<size_t> ord(k);
+            std::iota(ord.begin(), ord.end(), 0);
+            std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
+            sid.resize(k);
+            sv.resize(k);
+            for (size_t i = 0; i < k; ++i) {
+                sid[i] = ids[ord[i]];
+                sv[i] = vals[ord[i]];
+            }
+            ids.swap(sid);
+            vals.swap(sv);
+        } else {
+            by_id(ids, vals);
+        }
+        return;
     }
-    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ids[a] < ids[b]; });
-    std::vector<int64_t> ni(ord.size());
-    std::vector<double> nv(ord.size());
-    for (size_t i = 0; i < ord.size(); ++i) {
-        ni[i] = ids[ord[i]];
-        nv[i] = vals[ord[i]];
+    // key order: larger |v| first; NaN magnitudes last (numpy sorts NaN to
+    // the end); ties by smaller id
+    auto better = [](double ma, int64_t ia, double mb, int64_t ib) {
+        const bool na = std::isnan(ma), nb = std::isnan(mb);
+        if (na || nb) return na == nb ? ia < ib : nb;
+        if (ma != mb) return ma > mb;
+        return ia < ib;
+    };
+    sid.clear();
+    sv.clear();
+    thread_local std::vector<double> smag;
+    smag.clear();
+    for (size_t i = 0; i < k; ++i) {
+        const double mi = std::fabs(vals[i]);
+        const int64_t ii = ids[i];
+        if ((int64_t)sid.size() == p && !better(mi, ii, smag.back(), sid.back())) continue;
+        if ((int64_t)sid.size() < p) {
+            sid.push_back(ii);
+            sv.push_back(vals[i]);
+            smag.push_back(mi);
+        } else {
+            sid.back() = ii;
+            sv.back() = vals[i];
+            smag.back() = mi;
+        }
+        for (size_t b = sid.size() - 1; b > 0 && better(smag[b], sid[b], smag[b - 1], sid[b - 1]); --b) {
+            std::swap(sid[b], sid[b - 1]);
+            std::swap(sv[b], sv[b - 1]);
+            std::swap(smag[b], smag[b - 1]);
+        }
     }
-    ids.swap(ni);
-    vals.swap(nv);
+    ids.assign(sid.begin(), sid.end());
+    vals.assign(sv.begin(), sv.end());
+    by_id(ids, vals);
 }
 
 // CscMatrix.from_coo for entries without duplicates or zeros (the factor
@@ -150,88 +200,133 @@ int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *ptr, const int64_t *
     auto F = new rsb_ilup();
     F->m = m;
     F->n = n;
-    std::vector<int64_t> &row_at = F->row_at, &pos_of = F->pos_of, &rc = F->rc;
-    row_at.resize(m);
-    pos_of.resize(m);
-    std::iota(row_at.begin(), row_at.end(), 0);
-    std::iota(pos_of.begin(), pos_of.end(), 0);
-    rc.assign(m, 0);  // remaining_row_counts (il.py:153-156)
-    for (int64_t k = 0; k < ptr[n]; ++k) rc[ridx[k]]++;
+    if (m >= (int64_t)1 << 31) {
+        set_error("ilup_factorize: %lld rows exceed the int32 row index", (long long)m);
+        delete F;
+        return RSB_EINVAL;
+    }
+    // Per-row working state in one 16-byte record, so that touching a row of
+    // the column's pattern (mark, position, value, remaining count) costs one
+    // cache line: at config-4 size (m = 1.6e7) every pattern row is a miss.
+    // rcm = 2 * remaining_row_count + mark; a pivotal row also carries its
+    // L column (loff, llen), so the reach DFS goes row record -> L rows ->
+    // child records with no detour through a per-position pointer array.
+    struct alignas(32) RowSt {
+        double x;
+        int32_t pos;
+        int32_t rcm;
+        int64_t loff;
+        int32_t llen;
+        int32_t pad;
+    };
+    std::vector<RowSt> R(m);
+    std::vector<int32_t> row_at(m);
+    for (int64_t i = 0; i < m; ++i) {
+        R[i].x = 0.0;
+        R[i].pos = (int32_t)i;
+        R[i].rcm = 0;
+        R[i].loff = 0;
+        R[i].llen = 0;
+        row_at[i] = (int32_t)i;
+    }
+    for (int64_t k = 0; k < ptr[n]; ++k) R[ridx[k]].rcm += 2;  // remaining_row_counts (il.py:153-156)
     std::vector<double> col_inf(n, 0.0);  // np.maximum.reduceat(|A|) (il.py:235-238)
     for (int64_t j = 0; j < n; ++j)
         for (int64_t k = ptr[j]; k < ptr[j + 1]; ++k) col_inf[j] = std::max(col_inf[j], std::fabs(avals[k]));
 
-    // l_rows[q]: original row ids of L column q (order as kept), u per column
-    std::vector<int64_t> l_ptr(1, 0), l_rows;
-    std::vector<double> l_vals;
-    std::vector<std::vector<int64_t>> u_rows(n);
-    std::vector<std::vector<double>> u_vals(n);
+    // L columns (original row ids, as kept) and U columns (pivot positions,
+    // diagonal last), both appended column by column
+    std::vector<int64_t> l_ptr(1, 0), u_ptr(1, 0);
+    std::vector<int32_t> l_rows, u_rows;
+    std::vector<double> l_vals, u_vals;
+    l_ptr.reserve(n + 1);
+    u_ptr.reserve(n + 1);
+    l_rows.reserve((size_t)n * std::min<int64_t>(p, 12));
+    l_vals.reserve((size_t)n * std::min<int64_t>(p, 12));
+    u_rows.reserve((size_t)n * std::min<int64_t>(p + 1, 12));
+    u_vals.reserve((size_t)n * std::min<int64_t>(p + 1, 12));
 
-    std::vector<double> x(m, 0.0);
-    std::vector<char> mark(m, 0);
-    std::vector<int64_t> pattern, u_pos, cand, kept;
-    std::vector<double> u_val, cval, kept_v;
-    std::vector<int64_t> post, stack_node, stack_cur;
+    std::vector<int32_t> pattern, post, stack_node, stack_cur;
+    std::vector<int64_t> u_pos, cand_pos;
+    std::vector<int32_t> cand;
+    std::vector<double> u_val, cval;
+    std::vector<int64_t> sel_id;
+    std::vector<double> sel_v;
     int64_t nmod = 0;
+    auto mark_of = [&](int32_t r) { return R[r].rcm & 1; };
+    auto set_mark = [&](int32_t r) { R[r].rcm |= 1; };
+    // the children of a node about to be expanded are checked one after the
+    // other; start all their record loads at once
+    auto prefetch_children = [&](int32_t node) {
+        const int64_t lo = R[node].loff, hi = lo + R[node].llen;
+        for (int64_t e = lo; e < hi; ++e) __builtin_prefetch(&R[l_rows[e]]);
+    };
 
     for (int64_t j = 0; j < n; ++j) {
         const int64_t alo = ptr[j], ahi = ptr[j + 1], alen = ahi - alo;
-        for (int64_t k = alo; k < ahi; ++k) x[ridx[k]] = avals[k];
-        pattern.assign(ridx + alo, ridx + ahi);
+        for (int64_t k = alo; k < ahi; ++k) R[ridx[k]].x = avals[k];
+        pattern.clear();
         u_pos.clear();
         u_val.clear();
         if (j == 0 || alen == 0) {
-            for (int64_t k = alo; k < ahi; ++k) mark[ridx[k]] = 1;
+            for (int64_t k = alo; k < ahi; ++k) {
+                set_mark((int32_t)ridx[k]);
+                pattern.push_back((int32_t)ridx[k]);
+            }
         } else if (alen >= std::max<int64_t>(8, j / 8)) {
             // dense-ish column: sweep pivot positions in order (il.py:258-279)
-            for (int64_t k = alo; k < ahi; ++k) mark[ridx[k]] = 1;
+            for (int64_t k = alo; k < ahi; ++k) {
+                set_mark((int32_t)ridx[k]);
+                pattern.push_back((int32_t)ridx[k]);
+            }
             for (int64_t q = 0; q < j; ++q) {
-                const int64_t u = row_at[q];
-                const double xu = x[u];
+                const int32_t u = row_at[q];
+                const double xu = R[u].x;
                 if (xu == 0.0) continue;
                 u_pos.push_back(q);
                 u_val.push_back(xu);
                 for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
-                    const int64_t r = l_rows[e];
+                    RowSt &rr = R[l_rows[e]];
                     const double c = l_vals[e] * xu;
-                    x[r] = x[r] - c;
+                    rr.x = rr.x - c;
                 }
                 for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
-                    const int64_t r = l_rows[e];
-                    if (!mark[r]) {
-                        mark[r] = 1;
+                    const int32_t r = l_rows[e];
+                    if (!mark_of(r)) {
+                        set_mark(r);
                         pattern.push_back(r);
                     }
                 }
             }
         } else {
             // sparse column: DFS reach over the partial factor (il.py:170-208)
-            pattern.clear();
             post.clear();
             for (int64_t k = alo; k < ahi; ++k) {
-                const int64_t s = ridx[k];
-                if (mark[s]) continue;
-                mark[s] = 1;
+                const int32_t s = (int32_t)ridx[k];
+                if (mark_of(s)) continue;
+                set_mark(s);
                 pattern.push_back(s);
-                if (pos_of[s] >= j) continue;
+                if (R[s].pos >= j) continue;
                 stack_node.assign(1, s);
                 stack_cur.assign(1, 0);
+                prefetch_children(s);
                 while (!stack_node.empty()) {
-                    const int64_t node = stack_node.back();
-                    int64_t cursor = stack_cur.back();
-                    const int64_t q = pos_of[node];
-                    const int64_t clo = l_ptr[q], clen = l_ptr[q + 1] - clo;
+                    const int32_t node = stack_node.back();
+                    int32_t cursor = stack_cur.back();
+                    const int64_t clo = R[node].loff;
+                    const int32_t clen = R[node].llen;
                     bool advanced = false;
                     while (cursor < clen) {
-                        const int64_t child = l_rows[clo + cursor];
+                        const int32_t child = l_rows[clo + cursor];
                         ++cursor;
-                        if (!mark[child]) {
-                            mark[child] = 1;
+                        if (!mark_of(child)) {
+                            set_mark(child);
                             pattern.push_back(child);
-                            if (pos_of[child] < j) {
+                            if (R[child].pos < j) {
                                 stack_cur.back() = cursor;
                                 stack_node.push_back(child);
                                 stack_cur.push_back(0);
+                                prefetch_children(child);
                                 advanced = true;
                                 break;
                             }
@@ -246,32 +341,34 @@ int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *ptr, const int64_t *
             }
             // eliminate reached pivots in topological order (reversed post-order)
             for (auto it = post.rbegin(); it != post.rend(); ++it) {
-                const int64_t u = *it;
-                const double xu = x[u];
+                const int32_t u = *it;
+                const double xu = R[u].x;
                 if (xu == 0.0) continue;
-                const int64_t q = pos_of[u];
+                const int64_t q = R[u].pos;
                 u_pos.push_back(q);
                 u_val.push_back(xu);
-                for (int64_t e = l_ptr[q]; e < l_ptr[q + 1]; ++e) {
-                    const int64_t r = l_rows[e];
+                for (int64_t e = R[u].loff, ee = e + R[u].llen; e < ee; ++e) {
+                    RowSt &rr = R[l_rows[e]];
                     const double c = l_vals[e] * xu;
-                    x[r] = x[r] - c;
+                    rr.x = rr.x - c;
                 }
             }
         }
 
-        dual_drop(u_pos, u_val, p, tau);  // il.py:300
+        dual_drop_fast(u_pos, u_val, p, tau, sel_id, sel_v);  // il.py:300
 
         // active part: reached rows not yet pivotal, nonzero (il.py:303-307)
         cand.clear();
         cval.clear();
-        for (int64_t r : pattern)
-            if (pos_of[r] >= j && x[r] != 0.0) {
+        for (int32_t r : pattern) {
+            const RowSt &rr = R[r];
+            if (rr.pos >= j && rr.x != 0.0) {
                 cand.push_back(r);
-                cval.push_back(x[r]);
+                cval.push_back(rr.x);
             }
+        }
 
-        int64_t pivot_orig;
+        int32_t pivot_orig;
         double pivot_val;
         // modify_pivot (il.py:142-150)
         auto modified = [&]() {
@@ -299,17 +396,19 @@ int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *ptr, const int64_t *
             }
             const double thr = mu * mx;
             int64_t best = -1;
+            int32_t best_rc = 0, best_pos = 0;
             for (size_t i = 0; i < cand.size(); ++i) {
                 if (!(std::fabs(cval[i]) >= thr)) continue;
-                if (best < 0) {
+                const RowSt &rr = R[cand[i]];
+                const int32_t rc = rr.rcm >> 1;
+                if (best < 0 || rc < best_rc || (rc == best_rc && rr.pos < best_pos)) {
                     best = (int64_t)i;
-                    continue;
+                    best_rc = rc;
+                    best_pos = rr.pos;
                 }
-                const int64_t rb = rc[cand[best]], ri = rc[cand[i]];
-                if (ri < rb || (ri == rb && pos_of[cand[i]] < pos_of[cand[best]])) best = (int64_t)i;
             }
-            pivot_orig = row_at[pos_of[cand[best]]];
-            pivot_val = x[pivot_orig];
+            pivot_orig = cand[best];
+            pivot_val = R[pivot_orig].x;
             if (std::fabs(pivot_val) < small) {
                 pivot_val = modified();
                 ++nmod;
@@ -326,77 +425,94 @@ int rsb_ilup_factorize(int64_t m, int64_t n, const int64_t *ptr, const int64_t *
         }
 
         // interchange (il.py:324-328)
-        const int64_t q = pos_of[pivot_orig];
+        const int32_t q = R[pivot_orig].pos;
         if (q != j) {
-            const int64_t other = row_at[j];
+            const int32_t other = row_at[j];
             row_at[j] = pivot_orig;
             row_at[q] = other;
-            pos_of[pivot_orig] = j;
-            pos_of[other] = q;
+            R[pivot_orig].pos = (int32_t)j;
+            R[other].pos = q;
         }
 
         // scale, then drop in the L column by current position (il.py:331-339)
-        kept.clear();
-        kept_v.clear();
+        cand_pos.clear();
         for (size_t i = 0; i < cand.size(); ++i) {
-            kept.push_back(pos_of[cand[i]]);
-            kept_v.push_back(cval[i] / pivot_val);
+            cand_pos.push_back(R[cand[i]].pos);
+            cval[i] = cval[i] / pivot_val;
         }
-        dual_drop(kept, kept_v, p, tau);
-        for (size_t i = 0; i < kept.size(); ++i) {
-            l_rows.push_back(row_at[kept[i]]);
-            l_vals.push_back(kept_v[i]);
+        dual_drop_fast(cand_pos, cval, p, tau, sel_id, sel_v);
+        for (size_t i = 0; i < cand_pos.size(); ++i) {
+            l_rows.push_back(row_at[cand_pos[i]]);
+            l_vals.push_back(cval[i]);
         }
+        R[pivot_orig].loff = l_ptr.back();
+        R[pivot_orig].llen = (int32_t)(l_rows.size() - l_ptr.back());
         l_ptr.push_back((int64_t)l_rows.size());
 
-        u_rows[j] = u_pos;
-        u_rows[j].push_back(j);
-        u_vals[j] = u_val;
-        u_vals[j].push_back(pivot_val);
+        for (size_t i = 0; i < u_pos.size(); ++i) {
+            u_rows.push_back((int32_t)u_pos[i]);
+            u_vals.push_back(u_val[i]);
+        }
+        u_rows.push_back((int32_t)j);
+        u_vals.push_back(pivot_val);
+        u_ptr.push_back((int64_t)u_rows.size());
 
-        for (int64_t k = alo; k < ahi; ++k) rc[ridx[k]] -= 1;
-        for (int64_t r : pattern) {
-            x[r] = 0.0;
-            mark[r] = 0;
+        for (int64_t k = alo; k < ahi; ++k) R[ridx[k]].rcm -= 2;
+        for (int32_t r : pattern) {
+            R[r].x = 0.0;
+            R[r].rcm &= ~1;
         }
     }
     F->nmod = nmod;
-
-    // assemble in final pivot coordinates (il.py:349-359)
-    {
-        std::vector<int64_t> rr, cc;
-        std::vector<double> vv;
-        for (int64_t j = 0; j < n; ++j)
-            for (size_t k = 0; k < u_rows[j].size(); ++k) {
-                rr.push_back(u_rows[j][k]);
-                cc.push_back(j);
-                vv.push_back(u_vals[j][k]);
-            }
-        coo_to_csc(n, rr, cc, vv, F->u_ptr, F->u_idx, F->u_val);
+    F->row_at.assign(row_at.begin(), row_at.end());
+    F->pos_of.resize(m);
+    F->rc.resize(m);
+    for (int64_t i = 0; i < m; ++i) {
+        F->pos_of[i] = R[i].pos;
+        F->rc[i] = R[i].rcm >> 1;
     }
+    std::vector<RowSt>().swap(R);
+
+    // assemble in final pivot coordinates (il.py:349-359).  U: the rows of
+    // column j are positions < j (fixed once pivotal), ascending, then j --
+    // already CscMatrix.from_coo's sorted order.
+    F->u_ptr = u_ptr;
+    F->u_idx.assign(u_rows.begin(), u_rows.end());
+    F->u_val = u_vals;
     {
-        std::vector<int64_t> r1, c1, r2, c2;
-        std::vector<double> v1, v2;
-        for (int64_t j = 0; j < n; ++j)
-            for (int64_t e = l_ptr[j]; e < l_ptr[j + 1]; ++e) {
-                const int64_t pos = pos_of[l_rows[e]];
-                if (pos < n) {
-                    r1.push_back(pos);
-                    c1.push_back(j);
-                    v1.push_back(l_vals[e]);
+        // L: final positions, split at n, rows sorted inside each column
+        F->l1_ptr.assign(n + 1, 0);
+        F->l2_ptr.assign(n + 1, 0);
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t c1 = 0, c2 = 0;
+            for (int64_t e = l_ptr[j]; e < l_ptr[j + 1]; ++e) (F->pos_of[l_rows[e]] < n ? c1 : c2)++;
+            F->l1_ptr[j + 1] = F->l1_ptr[j] + c1;
+            F->l2_ptr[j + 1] = F->l2_ptr[j] + c2;
+        }
+        F->l1_idx.resize(F->l1_ptr[n]);
+        F->l1_val.resize(F->l1_ptr[n]);
+        F->l2_idx.resize(F->l2_ptr[n]);
+        F->l2_val.resize(F->l2_ptr[n]);
+        std::vector<std::pair<int64_t, double>> tmp;
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t d1 = F->l1_ptr[j], d2 = F->l2_ptr[j];
+            tmp.clear();
+            for (int64_t e = l_ptr[j]; e < l_ptr[j + 1]; ++e) tmp.emplace_back(F->pos_of[l_rows[e]], l_vals[e]);
+            std::sort(tmp.begin(), tmp.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
+            for (const auto &t : tmp) {
+                if (t.first < n) {
+                    F->l1_idx[d1] = t.first;
+                    F->l1_val[d1++] = t.second;
                 } else {
-                    r2.push_back(pos - n);
-                    c2.push_back(j);
-                    v2.push_back(l_vals[e]);
+                    F->l2_idx[d2] = t.first - n;
+                    F->l2_val[d2++] = t.second;
                 }
             }
-        coo_to_csc(n, r1, c1, v1, F->l1_ptr, F->l1_idx, F->l1_val);
-        coo_to_csc(n, r2, c2, v2, F->l2_ptr, F->l2_idx, F->l2_val);
+        }
     }
     *out = F;
     return RSB_OK;
 }
-
 int rsb_ilup_sizes(const rsb_ilup *F, int64_t *nnz_l1, int64_t *nnz_l2, int64_t *nnz_u, int64_t *nmod) {
     *nnz_l1 = (int64_t)F->l1_idx.size();
     *nnz_l2 = (int64_t)F->l2_idx.size();
