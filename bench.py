@@ -1,28 +1,37 @@
 """Benchmark of the B200 solve phase: preconditioned CGLS iterations/s.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 1]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4 --n N]
 
-A step is one preconditioned CGLS iteration of pcgls (sv.py:202-241) -- one
-product with A and A^T, one row-splitting preconditioner application, the
-dots and the scalar recursion -- on the BASELINE.json workload (config 1:
-256^2 grid, n = 65,536, m = 98,304, cg(2) coupling solve because s = 32,768
-exceeds the dense cap, mu = 1.0).  Inputs are the seeded
-synthetic generators of paper_2603_28642_b200/workloads.py.
+Workload (default): BASELINE.json configs[4] at its full size -- n = 8e6,
+m = 1.6e7, six nonzeros per row (~96M), rows permuted -- the largest
+configuration, and it fits one B200.  Setup follows the reference pipeline
+(cli.py:59-94): column_scale, power_method_norm2(100), ilup_factorize(p=10,
+tau=0, mu=1), build_preconditioner(cg(2), implicit Y: s = 8e6
+exceeds the dense cap), pcgls.  Dots follow the reference's OpenBLAS order
+on 64 threads (the order numpy uses on a 64-thread host; the single-thread
+order makes every 1.6e7-long dot one serial chain).
 
-The timed region is device time (CUDA events on the solver's stream) of K
-iterations run as replays of the captured iteration graph, with the L2
-flushed before every iteration outside the bracket; `e2e` is the same metric
-through the public API (pcgls with host buffers: H2D of b, D2H of x inside).
-Under torchrun each rank solves its own right-hand side on its own GPU
-(replicas, weak scaling; no collective on the data path); times are the max
-over ranks.  --impl reference times the CPU oracle port of the reference's
-pcgls on the same workload (the reference itself is pure Python/numpy and
-cannot travel to the GPU box).
+A step is one preconditioned CGLS iteration (sv.py:202-241): A p, A^T r, one
+row-splitting preconditioner application (8 sparse triangular solves, 3 L2
+and 3 L2^T products, the inner-CG dots), the outer dots and the scalar
+recursion.  `value` = iterations/s of one right-hand side, device time
+(CUDA events on the solver's stream, inputs resident, L2 flushed before
+every iteration outside the bracket); `e2e` = the same through the public
+pcgls() with b in pinned host memory and x returned; `rhs_batch` = the
+8-RHS-per-GPU shard of the 64-RHS batch through pcgls_batch.
+
+--impl reference times the reference's algorithm on the host cores: the
+oracle port (oracle/, bit-identical restatement; the reference package is
+pure Python and does not exist on the GPU box), set up with the oracle's
+own column_scale and ILUP -- no product code is loaded.  Both arms print
+the same `config`.  Under torchrun each rank solves its own right-hand
+side(s) (replicas, weak scaling); times are the max over ranks.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -42,26 +51,32 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--mu", type=float, default=1.0)
     ap.add_argument("--mode", default=None, help="coupling solve: dense | cg | identity")
     ap.add_argument("--grid", type=int, default=256, help="config 1 grid side")
-    ap.add_argument("--n", type=int, default=None, help="override n for configs 0/2/3/4")
+    ap.add_argument("--n", type=int, default=None, help="override n (default: the BASELINE size)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-tol", action="store_true", help="skip the time-to-tolerance run")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle comparison")
+    ap.add_argument("--parity-iters", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--batch", type=int, default=8,
-                    help="also time this many concurrent RHS per GPU through pcgls_batch (0: skip)")
-    ap.add_argument("--blas-threads", type=int, default=1,
+                    help="right-hand sides per GPU of the batched solve (0: skip)")
+    ap.add_argument("--blas-threads", type=int, default=None,
                     help="reproduce the reference's OpenBLAS dot order at this many threads "
-                         "(OPENBLAS_NUM_THREADS; 1 = the pinned single-thread order)")
+                         "(default: 64 for config 4, else 1)")
+    ap.add_argument("--cpu-threads", type=int, default=None,
+                    help="host threads of the oracle port (default: all cores)")
     ap.add_argument("--partition", default="replicas", choices=["replicas", "rows"],
-                    help="N>1: replicas (one RHS per GPU, weak) or rows (one RHS, A row-partitioned, "
-                         "NCCL allreduce of A^T r, strong)")
-    return ap.parse_args()
+                    help="N>1: replicas (RHS per GPU, weak) or rows (one RHS, row-partitioned, strong)")
+    a = ap.parse_args()
+    if a.blas_threads is None:
+        a.blas_threads = 64 if a.config == 4 else 1
+    return a
 
 
 def dist_env():
@@ -70,17 +85,32 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# workload
+# workload (shared by both arms: numpy generators only)
 # ---------------------------------------------------------------------------
 
 
-def make_workload(args, rank):
+def make_workload(args, rank, world):
+    """(A, b, B_batch, settings, name, generate_s).  b is this rank's single
+    right-hand side; B_batch its shard of the batch."""
     from paper_2603_28642_b200 import workloads as W
 
     cfgid = args.config
     st = dict(W.SETTINGS[cfgid])
     t0 = time.perf_counter()
-    if cfgid == 1:
+    Bb = None
+    if cfgid == 4:
+        n = args.n or 8_000_000
+        nb = max(0, args.batch)
+        # rank r: rhs 8r .. 8r+7 of the 64-RHS batch (its shard, rhs_batch);
+        # the single-RHS line solves the first of them
+        if nb:
+            A, Bb = W.config4(seed=4, n=n, nrhs=nb, first_rhs=rank * nb)
+            b = Bb[0]
+        else:
+            A, B1 = W.config4(seed=4, n=n, nrhs=1, first_rhs=rank)
+            b = B1[0]
+        name = f"config4: random sparse LS, n={A.ncols}, m={A.nrows}, nnz={A.nnz}"
+    elif cfgid == 1:
         A, b = W.config1(seed=1, g=args.grid)
         name = f"config1: {args.grid}x{args.grid} grid LS, n={A.ncols}, m={A.nrows}"
     elif cfgid == 0:
@@ -89,40 +119,63 @@ def make_workload(args, rank):
     elif cfgid == 2:
         A, b = W.config2(seed=2, **({} if args.n is None else dict(n=args.n)))
         name = f"config2: sparse + 100 dense rows, n={A.ncols}, m={A.nrows}"
-    elif cfgid == 3:
-        A, b = W.config3(seed=3, n=args.n or 100_000)
+    else:
+        A, b = W.config3(seed=3, n=args.n or 1_000_000)
         name = f"config3: ill-conditioned random LS, n={A.ncols}, m={A.nrows}"
-    else:
-        A, B = W.config4(seed=4, n=args.n or 1_000_000, nrhs=max(1, rank + 1))
-        b = B[rank]
-        name = f"config4 structure: n={A.ncols}, m={A.nrows}"
-    if rank > 0 and cfgid != 4:
-        # replicas: every rank solves its own right-hand side
-        b = b + 1e-3 * np.random.default_rng(1000 + rank).standard_normal(len(b))
-    t_gen = time.perf_counter() - t0
-    return A, b, st, name, t_gen
+    if cfgid != 4:
+        if rank > 0:  # replicas: every rank solves its own right-hand side
+            b = b + 1e-3 * np.random.default_rng(1000 + rank).standard_normal(len(b))
+        if args.batch > 0:
+            rng = np.random.default_rng(77 + rank)
+            Bb = np.stack([b] + [b + 1e-3 * rng.standard_normal(len(b)) for _ in range(args.batch - 1)])
+    return A, np.ascontiguousarray(b), Bb, st, name, time.perf_counter() - t0
 
 
-def setup(args, A, st):
-    import paper_2603_28642_b200 as P
-
-    times = {}
-    t0 = time.perf_counter()
-    if st["scale"]:
-        S, _ = P.column_scale(A)
-    else:
-        S = A
-    times["column_scale_s"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    f = P.ilup_factorize(S, P.IlupParams(p=st["p"], tau=st["tau"], mu=args.mu))
-    times["ilup_host_s"] = time.perf_counter() - t0
+def coupling_mode(args, st, s):
     mode = args.mode or st["s_mode"]
-    if mode == "dense" and f.L2.nrows > 20000:
+    if mode == "dense" and s > 20000:
         mode = "cg"  # the reference CLI's fallback (cli.py:68-78)
-    t0 = time.perf_counter()
-    pre = P.build_preconditioner(f, s_mode=P.SMode(mode))
-    times["build_preconditioner_s"] = time.perf_counter() - t0
-    return S, f, pre, mode, times
+    return mode
+
+
+def config_dict(args, st, name, nnz, mode):
+    """The `config` both arms print (identical by construction)."""
+    return {
+        "workload": name, "mu": args.mu, "p": st["p"], "tau": st["tau"], "coupling": mode,
+        "y_mode": "explicit" if mode == "dense" else "implicit", "cg_iters": 2,
+        "nnz": nnz, "delta": st["delta"], "max_iters": st["max_iters"],
+        "column_scale": bool(st["scale"]),
+        "dot_order": (f"reference OpenBLAS ddot association, {args.blas_threads} thread"
+                      f"{'s' if args.blas_threads > 1 else ''}"),
+        "rhs": "one per pcgls call (sv.py:120); batch shard of 8 per GPU under rhs_batch",
+    }
+
+
+def factor_digest(S_values, f):
+    h = hashlib.sha256()
+    for a in (S_values, f.row_perm.perm, f.L1.col_ptr, f.L1.row_idx, f.L1.values, f.L2.col_ptr,
+              f.L2.row_idx, f.L2.values, f.U.col_ptr, f.U.row_idx, f.U.values):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+def reference_hashes(args, S_values, scale, f):
+    """Compare with the digests of the REFERENCE's own setup, when committed
+    for this size (tests/golden/cfg4_factor_hashes.json)."""
+    if args.config != 4 or args.mu != 1.0:
+        return None
+    try:
+        with open(os.path.join(HERE, "tests", "golden", "cfg4_factor_hashes.json")) as fh:
+            want = json.load(fh).get(str(f.U.ncols))
+    except OSError:
+        return None
+    if not want:
+        return None
+    sys.path.insert(0, os.path.join(HERE, "tests", "golden"))
+    from make_cfg4_hashes import factor_digests
+
+    got = factor_digests(S_values, scale, f)
+    return all(got[k] == want[k] for k in got)
 
 
 # ---------------------------------------------------------------------------
@@ -144,10 +197,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.15)
         except OSError:
             self.proc = None
         return self
@@ -187,12 +241,11 @@ def tri_bytes(nnz, n):
     return 12 * nnz + 4 * (n + 1) + 16 * n
 
 
-def trsv_bytes_per_iteration(pre, mode):
-    f = pre.factors
+def trsv_bytes_per_iteration(f, mode, cg_iters=2):
     n, s = f.U.ncols, f.L2.nrows
     l1 = tri_bytes(f.L1.nnz, n)
     u = tri_bytes(f.U.nnz, n)
-    k = pre.cg_iters
+    k = cg_iters
     if s == 0:
         return l1 + u, {"L1": 1, "L1T": 0, "U": 1}
     if mode == "cg":
@@ -208,81 +261,138 @@ def measured_peak():
     path = os.path.join(HERE, "MEASURED_PEAKS.json")
     try:
         with open(path) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
-        return FALLBACK_HBM_GBS, "fallback"
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """DRAM bytes (read + write) per iteration of the dominant kernel class,
-    summed over the iteration's solves, from the committed ncu capture
-    (profiles/ncu_trsv_r01.json), or None."""
-    path = os.path.join(HERE, "profiles", "ncu_trsv_r01.json")
+def ncu_traffic(workload_key):
+    """DRAM bytes (read + write) per iteration of the dominant kernel class
+    from the committed ncu capture of this workload, or (None, why)."""
+    path = os.path.join(HERE, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d.get("dram_bytes_per_iteration"), d.get("source")
+            d = json.load(fh).get(workload_key)
+        if d:
+            return d.get("dram_bytes_per_iteration"), d.get("source")
     except (OSError, ValueError):
-        return None, None
+        pass
+    return None, "no ncu capture committed for this workload"
+
+
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        cores = os.cpu_count()
+    return model, cores
 
 
 # ---------------------------------------------------------------------------
-# arms
+# reference arm: the oracle port on the host cores, no product code
 # ---------------------------------------------------------------------------
 
 
-CPU_THREADS_NOTE = ("one core: the reference solve is sequential (triangular solves, np.add.at / reduceat scatters in numpy); only its BLAS dots could use more threads, and the port runs them in the reference's one-thread OpenBLAS order (--blas-threads T selects the T-thread order)")
-
-
-def cpu_oracle_rate(S, pre, b, norm_a, budget_s, max_iters_cap=400):
-    """Oracle port of pcgls (oracle/oracle.py), single thread, fixed-iteration
-    run sized to roughly budget_s seconds; returns (iters/s, iters, seconds)."""
+def oracle_setup(args, A, st):
     from oracle import oracle as O
 
-    op = O.OraclePreconditioner.from_reference(pre)
-    O.set_blas_threads(int(os.environ.get("RSB_BLAS_THREADS", "1")))
     t0 = time.perf_counter()
-    O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=2)
-    probe = max(time.perf_counter() - t0, 1e-4) / 2
-    k = int(max(3, min(max_iters_cap, budget_s / probe)))
+    if st["scale"]:
+        S, scale = O.column_scale(A)
+    else:
+        S, scale = A, np.ones(A.ncols)
+    t_scale = time.perf_counter() - t0
     t0 = time.perf_counter()
-    O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=k)
-    dt = time.perf_counter() - t0
-    return k / dt, k, dt
+    f = O.ilup_factorize(S, p=st["p"], tau=st["tau"], mu=args.mu)
+    t_ilup = time.perf_counter() - t0
+    return S, scale, f, {"column_scale_s": t_scale, "ilup_s": t_ilup}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     from oracle import oracle as O
 
+    model, cores = host_cpu()
+    threads = args.cpu_threads or cores
     O.set_blas_threads(args.blas_threads)
-
-    A, b, st, name, _ = make_workload(args, 0)
-    S, f, pre, mode, _ = setup(args, A, st)
+    O.set_cpu_threads(threads)
+    A, b, _, st, name, t_gen = make_workload(args, 0, 1)
+    S, scale, f, times = oracle_setup(args, A, st)
+    mode = coupling_mode(args, st, f.L2.nrows)
+    if mode == "dense":
+        raise SystemExit("reference arm: dense coupling needs the explicit Y/S build (use --mode cg)")
+    t0 = time.perf_counter()
     norm_a = O.power_method_norm2(S, 100, args.config)
-    # warmup + K steps, each step one iteration; bounded sample
-    op = O.OraclePreconditioner.from_reference(pre)
-    O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=max(1, min(args.warmup, 3)))
+    times["power_method_s"] = time.perf_counter() - t0
+    op = O.OraclePreconditioner(f, mode, "implicit", 2)
+    O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=max(1, args.warmup))
     k = args.steps
     t0 = time.perf_counter()
-    O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=k)
+    _, rep = O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=k)
     dt = time.perf_counter() - t0
     value = k / dt
+    nnz = {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz}
+    sample = (f"{k} fixed iterations (delta=1e-300) of the oracle port of pcgls on this config "
+              f"after {args.warmup} warm-up iterations")
     line = {
         "impl": "reference", "metric": "preconditioned CGLS iterations/s", "value": value,
         "unit": "iter/s", "n_gpus": args.gpus, "steps": k, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded generators, workloads.py)",
-        "config": {"workload": name, "mu": args.mu, "coupling": mode, "p": st["p"], "tau": st["tau"]},
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port",
-                         "sample": f"{k} fixed iterations (delta=1e-300) of the oracle port of pcgls",
-                         "threads": CPU_THREADS_NOTE},
+        "dtype": "f64", "data": "synthetic (seeded generators, paper_2603_28642_b200/workloads.py)",
+        "config": config_dict(args, st, name, nnz, mode),
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": threads, "kind": "port",
+                         "sample": sample, "host_cpu": model, "host_cores": cores},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup": {**times, "generate_s": t_gen, "factor_digest": factor_digest(S.values, f)},
+        "native_libs": loaded_native_libs(),
     }
     print(json.dumps(line), flush=True)
+
+
+def loaded_native_libs():
+    try:
+        with open("/proc/self/maps") as fh:
+            libs = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so") and HERE in ln}
+        return sorted(os.path.relpath(p, HERE) for p in libs)
+    except OSError:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+
+def product_setup(args, A, st):
+    import paper_2603_28642_b200 as P
+
+    times = {}
+    t0 = time.perf_counter()
+    if st["scale"]:
+        S, sc = P.column_scale(A)
+        scale = sc.scale
+    else:
+        S, scale = A, np.ones(A.ncols)
+    times["column_scale_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    f = P.ilup_factorize(S, P.IlupParams(p=st["p"], tau=st["tau"], mu=args.mu))
+    times["ilup_host_s"] = time.perf_counter() - t0
+    mode = coupling_mode(args, st, f.L2.nrows)
+    t0 = time.perf_counter()
+    pre = P.build_preconditioner(f, s_mode=P.SMode(mode))
+    times["build_preconditioner_s"] = time.perf_counter() - t0
+    return S, scale, f, pre, mode, times
 
 
 def run_b200(args):
@@ -311,28 +421,29 @@ def run_b200(args):
 
     import paper_2603_28642_b200 as P
     from paper_2603_28642_b200 import _lib as L
-    from paper_2603_28642_b200.device import (DeviceBuffer, PinnedBuffer, device_matrix,
-                                              device_preconditioner, device_solver, get_context)
+    from paper_2603_28642_b200 import device as D
 
-    A, b, st, name, t_gen = make_workload(args, rank)
-    S, f, pre, mode, times = setup(args, A, st)
-    ctx = get_context()
+    A, b, Bb, st, name, t_gen = make_workload(args, rank, world)
+    S, scale, f, pre, mode, times = product_setup(args, A, st)
+    ctx = D.get_context()
     t0 = time.perf_counter()
-    dA = device_matrix(S, ctx)
-    dpre = device_preconditioner(pre, ctx)
-    solver = device_solver(dA, dpre)
+    dA = D.device_matrix(S, ctx)
+    dpre = D.device_preconditioner(pre, ctx)
+    solver = D.device_solver(dA, dpre)
+    ctx.sync()
+    times["upload_and_analysis_s"] = time.perf_counter() - t0
     lv_l1 = dpre.L1.levels(L.TRI_LOWER_UNIT)
     lv_u = dpre.U.levels(L.TRI_UPPER)
-    variants = {"L1": dpre.L1.variant(L.TRI_LOWER_UNIT), "L1T": dpre.L1.variant(L.TRI_LOWER_T_UNIT),
-                "U": dpre.U.variant(L.TRI_UPPER)}
-    times["upload_and_analysis_s"] = time.perf_counter() - t0
+    variants = {"L1": dpre.L1.variant(L.TRI_LOWER_UNIT), "U": dpre.U.variant(L.TRI_UPPER)}
+    if f.L2.nrows:
+        variants["L1T"] = dpre.L1.variant(L.TRI_LOWER_T_UNIT)
     t0 = time.perf_counter()
     norm_a = P.power_method_norm2(S, 100, args.config)
     times["power_method_device_s"] = time.perf_counter() - t0
 
     K, Wm = args.steps, args.warmup
-    # ---- device-resident timed region
-    bdev = DeviceBuffer(ctx, len(b))
+    # ---- device-resident timed region: K iterations as graph replays
+    bdev = D.DeviceBuffer(ctx, len(b))
     bdev.upload(b)
     cfg = solver.cfg_struct(norm_a, 1e-300, Wm + K + 8, 5, False)
     status = solver.start(bdev.ptr, L.RSB_DEVICE, cfg)
@@ -340,7 +451,7 @@ def run_b200(args):
         raise RuntimeError(f"solver stopped at start (status {status})")
     solver.iterate(Wm)
     it_ms, tri_ms = np.zeros(1), np.zeros(1)
-    tri_launches, kpi, st_out = (np.zeros(1, dtype=np.int64) for _ in range(3))
+    tri_launches, kpi = np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)
     barrier()
     with ClockSampler(local) as clocks:
         st_c = np.zeros(1, dtype=np.int32)
@@ -355,64 +466,100 @@ def run_b200(args):
     value = world * K / (iter_ms_max / 1e3)
 
     # ---- end to end through the public API (host buffers, copies inside)
-    bpin = PinnedBuffer(len(b))
+    bpin = D.PinnedBuffer(len(b))
     bpin.array[:] = b
     e2e_cfg = P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=K)
     P.pcgls(S, bpin.array, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
     barrier()
     t0 = time.perf_counter()
-    x, rep = P.pcgls(S, bpin.array, pre, e2e_cfg)
+    x_e2e, rep = P.pcgls(S, bpin.array, pre, e2e_cfg)
     e2e_s = barrier_max(time.perf_counter() - t0)
-    e2e = world * rep.its / e2e_s if not rep.converged else world * K / e2e_s
+    e2e = world * K / e2e_s
 
-    # ---- several independent RHS per GPU, solved concurrently
+    # ---- the batch shard of right-hand sides per GPU
     batch = None
-    if args.batch > 1:
-        rng = np.random.default_rng(77 + rank)
-        Bm = np.stack([b] + [b + 1e-3 * rng.standard_normal(len(b)) for _ in range(args.batch - 1)])
-        P.pcgls_batch(S, Bm, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
+    if Bb is not None and len(Bb) > 1:
+        P.pcgls_batch(S, Bb, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
         barrier()
         t0 = time.perf_counter()
-        _, breps = P.pcgls_batch(S, Bm, pre, e2e_cfg)
+        _, breps = P.pcgls_batch(S, Bb, pre, e2e_cfg)
         b_s = barrier_max(time.perf_counter() - t0)
         its = sum(K if r.converged else r.its for r in breps)
-        batch = {"rhs_per_gpu": args.batch, "value": world * its / b_s, "unit": "RHS-iter/s",
-                 "seconds": b_s,
-                 "call": f"pcgls_batch(A, B[{args.batch} x m] host, pre, CglsConfig(delta=1e-300, "
-                         f"max_iters={K})): one stream + workspace per RHS, shared A and factors; all RHS "
-                         f"iterate concurrently when the solves are single-CTA, two at a time when "
-                         f"they are grid-wide (each fills most of the GPU)"}
+        batch = {"rhs_per_gpu": len(Bb), "value": world * its / b_s, "unit": "RHS-iter/s",
+                 "seconds": b_s, "its_each": K,
+                 "call": f"pcgls_batch(A, B[{len(Bb)} x m] host, pre, CglsConfig(delta=1e-300, "
+                         f"max_iters={K})), H2D of B and D2H of X inside"}
 
-    # ---- time to tolerance (config delta), device path, reported alongside
+    # ---- time to tolerance: power method + upload + level analysis + solve
     tol = None
     if not args.no_tol:
+        D.clear_caches()
+        dA = dpre = solver = None
         t0 = time.perf_counter()
+        D.device_matrix(S, ctx)
+        D.device_preconditioner(pre, ctx)
+        ctx.sync()
+        t_up = time.perf_counter() - t0
         nrm = P.power_method_norm2(S, 100, args.config)
-        _, rtol = P.pcgls(S, b, pre, P.CglsConfig(norm_A=nrm, delta=st["delta"], max_iters=st["max_iters"]))
-        tol = {"seconds": barrier_max(time.perf_counter() - t0), "its": rtol.its,
+        t_pm = time.perf_counter() - t0 - t_up
+        x_tol, rtol = P.pcgls(S, b, pre, P.CglsConfig(norm_A=nrm, delta=st["delta"], max_iters=st["max_iters"]))
+        t_all = barrier_max(time.perf_counter() - t0)
+        tol = {"seconds": t_all, "upload_and_analysis_s": t_up, "power_method_s": t_pm,
+               "solve_s": t_all - t_up - t_pm, "its": rtol.its,
                "converged": rtol.converged, "breakdown": rtol.breakdown, "delta": st["delta"],
                "ratio_pt_final": rtol.ratio_pt_final,
                "grad_ratio": rtol.gradient_norm_final / (nrm * rtol.residual_norm_final)
                if rtol.residual_norm_final > 0 else 0.0,
-               "includes": "power method (100 its) + pcgls to delta, host b in / x out"}
+               "includes": "upload + triangular-solve level analysis + power method (100 its) + pcgls "
+                           "to delta with host b in / x out; ILUP and build are in `setup`"}
 
     if rank != 0:
+        if dist is not None:
+            dist[1].destroy_process_group()
         return
     # ---- roofline of the dominant kernel class (the triangular solves)
-    tbytes, counts = trsv_bytes_per_iteration(pre, mode)
-    ntri = int(tri_launches[0])
+    tbytes, counts = trsv_bytes_per_iteration(f, mode)
     achieved = (tbytes * K) / (tri_ms[0] / 1e3) / 1e9
     peak, peak_kind = measured_peak()
-    traffic, traffic_src = ncu_traffic()
-    if not (args.config == 1 and args.grid == 256 and args.mu == 1.0 and mode == "cg"):
-        traffic, traffic_src = None, "no ncu capture committed for this workload"
-    cpu = None
-    if world == 1:
-        rate, kc, dtc = cpu_oracle_rate(S, pre, b, norm_a, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "iter/s", "cores": 1, "kind": "port",
-               "sample": f"{kc} fixed iterations (delta=1e-300) of the oracle port of pcgls on the same "
-                         f"workload, {dtc:.1f} s, host has {os.cpu_count()} cores",
-               "threads": CPU_THREADS_NOTE}
+    wkey = f"config{args.config}_n{S.ncols}_mu{args.mu}_{mode}"
+    traffic, traffic_src = ncu_traffic(wkey)
+    model, cores = host_cpu()
+
+    # ---- parity against the oracle port + the CPU baseline (rank 0, N = 1)
+    parity, cpu = None, None
+    if world == 1 and not args.no_parity and mode != "dense":
+        from oracle import oracle as O
+
+        threads = args.cpu_threads or max(1, cores - 1)
+        O.set_blas_threads(args.blas_threads)
+        O.set_cpu_threads(threads)
+        t0 = time.perf_counter()
+        norm_o = O.power_method_norm2(S, 100, args.config)
+        t_pm_o = time.perf_counter() - t0
+        op = O.OraclePreconditioner(f, mode, "implicit", 2)
+        kp = max(1, args.parity_iters)
+        t0 = time.perf_counter()
+        xo, ro = O.pcgls(S, b, op, norm_o, delta=1e-300, max_iters=kp)
+        t_o = time.perf_counter() - t0
+        xg, rg = P.pcgls(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=kp))
+        parity = {"iters": kp, "norm_A_bitwise": norm_a == norm_o, "x_bitwise": bool(np.array_equal(xg, xo)),
+                  "report_equal": rg.to_dict() == ro,
+                  "factors_match_reference_hashes": reference_hashes(args, S.values, scale, f),
+                  "factor_digest": factor_digest(S.values, f),
+                  "checker": "oracle port (oracle/), same scaled A, factors and b; fixed-iteration pcgls"}
+        # CPU baseline: a bounded sample of the same workload on the host cores
+        rate = kp / t_o
+        if t_o < args.cpu_seconds:
+            kc = int(max(kp, min(400, args.cpu_seconds / max(t_o / kp, 1e-4))))
+            t0 = time.perf_counter()
+            O.pcgls(S, b, op, norm_o, delta=1e-300, max_iters=kc)
+            t_o, kp = time.perf_counter() - t0, kc
+            rate = kc / t_o
+        cpu = {"value": rate, "unit": "iter/s", "cores": threads, "kind": "port",
+               "sample": f"{kp} fixed iterations (delta=1e-300) of the oracle port of pcgls on this config, "
+                         f"{t_o:.1f} s (power method {t_pm_o:.1f} s not included)",
+               "host_cpu": model, "host_cores": cores}
+
     line = {
         "metric": "preconditioned CGLS iterations/s",
         "value": value,
@@ -426,27 +573,25 @@ def run_b200(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generators, paper_2603_28642_b200/workloads.py)",
-        "config": {
-            "workload": name, "mu": args.mu, "p": st["p"], "tau": st["tau"], "coupling": mode,
-            "y_mode": pre.y_mode.value, "cg_iters": pre.cg_iters,
-            "nnz": {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz},
+        "config": config_dict(args, st, name, {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz}, mode),
+        "device": {
             "levels": {"L1": lv_l1[0], "U": lv_u[0], "L1_max_width": lv_l1[1], "U_max_width": lv_u[1]},
+            "trsv_kernels": {k: v[0] + (f"<N={v[1]}>" if v[1] else "") for k, v in variants.items()},
             "l2": "flushed (320 MiB write) before every timed iteration, outside the event bracket"
                   if not args.no_flush else "not flushed",
-            "parallelism": f"replicas x{world} (one RHS per GPU)",
-            "dot_order": (f"exact (reference OpenBLAS association, {args.blas_threads} thread"
-                          f"{'s' if args.blas_threads > 1 else ''})"),
+            "parallelism": f"replicas x{world}",
         },
         "roofline": {
-            "kernel": "triangular solves (+ k_gather_pos), 8 per cg(2) iteration: "
-                      + ", ".join(f"{k}: k_trsv_{v[0]}" + (f"<N={v[1]}>" if v[1] else "") for k, v in variants.items()),
+            "kernel": f"sparse triangular solves, {sum(counts.values())} per iteration ({counts})",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
             "traffic_source": traffic_src,
-            "algorithmic_bytes_per_iteration": tbytes, "launches_per_iteration": counts,
+            "algorithmic_bytes_per_iteration": tbytes,
             "share_of_step": float(tri_ms[0] / it_ms[0]),
+            "iteration_gbs_algorithmic": None,
         },
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": 8 * S.nrows / K,
                 "d2h_bytes_per_step": 8 * S.ncols / K,
                 "call": f"pcgls(A, b_pinned_host, pre, CglsConfig(delta=1e-300, max_iters={K})); "
@@ -457,38 +602,37 @@ def run_b200(args):
         "rhs_batch": batch,
         "time_to_tol": tol,
         "setup": {**times, "generate_s": t_gen},
-        "tri_launches_timed": ntri,
     }
     print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist[1].destroy_process_group()
 
 
 def run_rows(args):
-    """One RHS, A row-block partitioned across the ranks:
-    host-driven iteration with an NCCL allreduce of the n-vector per A^T
-    product and an allgather of r for the (replicated) preconditioner apply."""
+    """One RHS, A and L2 row-block partitioned across the ranks."""
     import torch
     import torch.distributed as tdist
 
     import paper_2603_28642_b200 as P
-    from paper_2603_28642_b200 import distributed as D
+    from paper_2603_28642_b200 import distributed as DI
 
     rank, world, local = dist_env()
     os.environ.setdefault("RSB_DEVICE", str(local))
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl")
-    A, b, st, name, _ = make_workload(args, 0)
-    S, f, pre, mode, times = setup(args, A, st)
+    A, b, _, st, name, _ = make_workload(args, 0, 1)
+    S, scale, f, pre, mode, times = product_setup(args, A, st)
     norm_a = P.power_method_norm2(S, 100, args.config)
-    comm = D.TorchComm(device=torch.device("cuda", local))
-    mk = lambda Al, pr: D.DeviceBackend(Al, pr, local)  # noqa: E731
-    D.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=args.warmup),
-                            comm, mk)
+    comm = DI.TorchComm(device=torch.device("cuda", local))
+    mk = lambda Al, pr: DI.DeviceBackend(Al, pr, local)  # noqa: E731
+    DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=args.warmup),
+                             comm, mk)
     K = args.steps
     torch.cuda.synchronize()
     tdist.barrier()
     t0 = time.perf_counter()
-    _, rep = D.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=K),
-                                     comm, mk)
+    _, rep = DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=K),
+                                      comm, mk)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
@@ -500,10 +644,9 @@ def run_rows(args):
             "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(1, rep.iters_run),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, paper_2603_28642_b200/workloads.py)",
-            "config": {"workload": name, "mu": args.mu, "coupling": mode,
-                       "parallelism": f"rows x{world}: A row-partitioned, NCCL allreduce of A^T r, "
-                                      "allgather of r, replicated apply",
-                       "timing": "wall clock around the fixed-iteration solve, max over ranks"},
+            "config": config_dict(args, st, name, {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz},
+                                  mode),
+            "parallelism": f"rows x{world}",
         }), flush=True)
     tdist.destroy_process_group()
 

@@ -65,6 +65,32 @@ def lib():
         L.rso_pairwise_sum.restype = f64
         L.rso_blas_dot.argtypes = [i64, _f64p, _f64p]
         L.rso_blas_dot.restype = f64
+        # rsfast.c (threaded evaluation, same bits)
+        L.rsf_csr.argtypes = [i64, i64, _i64p, _i64p, _f64p, _i64p, _i64p, _f64p]
+        L.rsf_matvec_csr.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p]
+        L.rsf_matvec_t.argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p, i64]
+        L.rsf_levels.argtypes = [i64, _i64p, _i64p, ctypes.c_int, _i64p, _i64p]
+        L.rsf_levels.restype = i64
+        for nm in ("rsf_lower_unit", "rsf_upper", "rsf_lower_t_unit"):
+            getattr(L, nm).argtypes = [i64, _i64p, _i64p, _f64p, _f64p, _f64p, i64, _i64p, _i64p]
+        L.rsf_dot.argtypes = [i64, _f64p, _f64p, ctypes.c_int]
+        L.rsf_dot.restype = f64
+        L.rsf_axpy.argtypes = [i64, _f64p, f64, _f64p, ctypes.c_int]
+        L.rsf_xpby.argtypes = [i64, _f64p, _f64p, f64, _f64p]
+        L.rsf_gather.argtypes = [i64, _f64p, _f64p, _i64p]
+        L.rsf_sub.argtypes = [i64, _f64p, _f64p, _f64p]
+        L.rsf_add.argtypes = [i64, _f64p, _f64p, _f64p]
+        L.rsf_copy.argtypes = [i64, _f64p, _f64p]
+        L.rsf_scale_div.argtypes = [i64, _f64p, _f64p, f64]
+        L.rsf_max_threads.restype = ctypes.c_int
+        L.rsf_set_threads.argtypes = [ctypes.c_int]
+        # ilupref.c
+        L.orc_ilup_factorize.argtypes = [i64, i64, _i64p, _i64p, _f64p, i64, f64, f64, f64,
+                                         ctypes.POINTER(ctypes.c_void_p), _i64p]
+        L.orc_ilup_sizes.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _i64p]
+        L.orc_ilup_copy.argtypes = [ctypes.c_void_p] + [_i64p, _i64p, _i64p, _i64p, _f64p, _i64p, _i64p,
+                                                        _f64p, _i64p, _i64p, _f64p]
+        L.orc_ilup_free.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -92,6 +118,158 @@ def _vec(v, n):
 
 
 # ---------------------------------------------------------------------------
+# threaded evaluation (rsfast.c): the same bits on all host cores
+# ---------------------------------------------------------------------------
+
+_cpu_threads = int(os.environ.get("RSB_ORACLE_THREADS", "1") or 1)
+
+
+def set_cpu_threads(t: int) -> int:
+    """Host threads the oracle kernels use (1 = the sequential restatement).
+    Results are bit-identical either way; returns the previous value."""
+    global _cpu_threads
+    prev, _cpu_threads = _cpu_threads, max(1, int(t))
+    lib().rsf_set_threads(_cpu_threads)
+    return prev
+
+
+def available_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
+class _Prep:
+    """Per-matrix data of the threaded kernels: the CSC arrays, a CSR copy
+    and the dependency levels of each solve kind, built on first use."""
+
+    def __init__(self, M):
+        self.M = M  # keeps id(M) unique while cached
+        self.m, self.n, self.cp, self.ri, self.va = _csc(M)
+        self.maxcol = int(np.diff(self.cp).max()) if self.n else 0
+        self._csr = None
+        self._lev = {}
+        self._upper_ok = None
+
+    def csr(self):
+        if self._csr is None:
+            nnz = int(self.cp[-1])
+            rp, ci, rv = np.empty(self.m + 1, dtype=np.int64), np.empty(nnz, dtype=np.int64), np.empty(nnz)
+            lib().rsf_csr(self.m, self.n, _p64(self.cp), _p64(self.ri), _pf(self.va), _p64(rp), _p64(ci), _pf(rv))
+            self._csr = (rp, ci, rv)
+        return self._csr
+
+    def upper_ok(self):
+        """every column's last stored entry is a nonzero diagonal (else the
+        sequential path raises LinAlgError as the reference does)"""
+        if self._upper_ok is None:
+            cp, ri, va = self.cp, self.ri, self.va
+            last = cp[1:] - 1
+            ok = self.m == self.n and bool(np.all(cp[1:] > cp[:-1]))
+            if ok:
+                ok = bool(np.all(ri[last] == np.arange(self.n))) and bool(np.all(va[last] != 0.0))
+            self._upper_ok = ok
+        return self._upper_ok
+
+    def levels(self, kind):
+        if kind not in self._lev:
+            if kind == 2:
+                ptr, idx = self.cp, self.ri
+            else:
+                ptr, idx = self.csr()[0], self.csr()[1]
+            order = np.empty(self.n, dtype=np.int64)
+            lp = np.empty(self.n + 1, dtype=np.int64)
+            nl = lib().rsf_levels(self.n, _p64(ptr), _p64(idx), kind, _p64(order), _p64(lp))
+            self._lev[kind] = (int(nl), order, lp)
+        return self._lev[kind]
+
+    def solve(self, kind, b):
+        """kind 0: unit lower (strict lower L), 1: upper, 2: unit lower transpose"""
+        b = _vec(b, self.n)
+        x = np.empty(self.n)
+        nl, order, lp = self.levels(kind)
+        if kind == 2:
+            lib().rsf_lower_t_unit(self.n, _p64(self.cp), _p64(self.ri), _pf(self.va), _pf(b), _pf(x), nl,
+                                   _p64(order), _p64(lp))
+        else:
+            rp, ci, rv = self.csr()
+            fn = lib().rsf_lower_unit if kind == 0 else lib().rsf_upper
+            fn(self.n, _p64(rp), _p64(ci), _pf(rv), _pf(b), _pf(x), nl, _p64(order), _p64(lp))
+        return x
+
+
+_preps: dict = {}
+
+
+def _prep(M):
+    P = _preps.get(id(M))
+    if P is None or P.M is not M:
+        P = _preps[id(M)] = _Prep(M)
+    return P
+
+
+def clear_prep_cache():
+    _preps.clear()
+
+
+# elementwise steps of the loops below, one IEEE operation per element as
+# numpy performs them; threaded when _cpu_threads > 1
+def _axpy(y, a, x, sign):
+    """y += a*x (sign +1) / y -= a*x (sign -1), in place"""
+    if _cpu_threads > 1:
+        lib().rsf_axpy(len(y), _pf(y), float(a), _pf(x), sign)
+    elif sign > 0:
+        y += a * x
+    else:
+        y -= a * x
+
+
+def _xpby(h, beta, p):
+    """h + beta*p (new array)"""
+    if _cpu_threads > 1:
+        out = np.empty(len(h))
+        lib().rsf_xpby(len(h), _pf(out), _pf(h), float(beta), _pf(p))
+        return out
+    return h + beta * p
+
+
+def _add(a, b):
+    if _cpu_threads > 1:
+        a, b = np.ascontiguousarray(a, dtype=np.float64), np.ascontiguousarray(b, dtype=np.float64)
+        out = np.empty(len(a))
+        lib().rsf_add(len(a), _pf(out), _pf(a), _pf(b))
+        return out
+    return a + b
+
+
+def _sub(a, b):
+    if _cpu_threads > 1:
+        a, b = np.ascontiguousarray(a, dtype=np.float64), np.ascontiguousarray(b, dtype=np.float64)
+        out = np.empty(len(a))
+        lib().rsf_sub(len(a), _pf(out), _pf(a), _pf(b))
+        return out
+    return a - b
+
+
+def _copy(a):
+    if _cpu_threads > 1:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.empty(len(a))
+        lib().rsf_copy(len(a), _pf(out), _pf(a))
+        return out
+    return np.array(a, dtype=np.float64, copy=True)
+
+
+def _gather(r, perm):
+    if _cpu_threads > 1:
+        out = np.empty(len(perm))
+        lib().rsf_gather(len(perm), _pf(out), _pf(r), _p64(perm))
+        return out
+    return r[perm]
+
+
+# ---------------------------------------------------------------------------
 # kernels (sc.py)
 # ---------------------------------------------------------------------------
 
@@ -101,6 +279,11 @@ def matvec(A, x):
     m, n, cp, ri, va = _csc(A)
     x = _vec(x, n)
     y = np.empty(m)
+    if _cpu_threads > 1:
+        P = _prep(A)
+        rp, ci, rv = P.csr()
+        lib().rsf_matvec_csr(m, _p64(rp), _p64(ci), _pf(rv), _pf(x), _pf(y))
+        return y
     lib().rso_matvec(m, n, _p64(cp), _p64(ri), _pf(va), _pf(x), _pf(y))
     return y
 
@@ -110,6 +293,10 @@ def matvec_transpose(A, y):
     m, n, cp, ri, va = _csc(A)
     y = _vec(y, m)
     z = np.empty(n)
+    if _cpu_threads > 1:
+        P = _prep(A)
+        lib().rsf_matvec_t(n, _p64(P.cp), _p64(P.ri), _pf(P.va), _pf(y), _pf(z), P.maxcol)
+        return z
     scratch = np.empty(max(1, int(np.diff(cp).max()) if n else 1))
     lib().rso_matvec_transpose(m, n, _p64(cp), _p64(ri), _pf(va), _pf(y), _pf(z), _pf(scratch))
     return z
@@ -129,16 +316,22 @@ def _tri(fn, T, b, *extra):
 
 def sparse_lower_solve(L, b, unit_diag=False):
     """sc.py:243-263."""
+    if _cpu_threads > 1 and unit_diag:
+        return _prep(L).solve(0, b)
     return _tri(lib().rso_lower_solve, L, b, int(bool(unit_diag)))
 
 
 def sparse_upper_solve(U, b):
     """sc.py:266-279."""
+    if _cpu_threads > 1 and _prep(U).upper_ok():
+        return _prep(U).solve(1, b)
     return _tri(lib().rso_upper_solve, U, b)
 
 
 def sparse_lower_solve_transpose(L, b, unit_diag=False):
     """sc.py:282-298."""
+    if _cpu_threads > 1 and unit_diag and _prep(L).maxcol <= 256:
+        return _prep(L).solve(2, b)
     return _tri(lib().rso_lower_solve_transpose, L, b, int(bool(unit_diag)))
 
 
@@ -205,6 +398,8 @@ def dot(a, b):
     widths = blas_chunks(len(a), _blas_threads)
     if len(widths) == 1:
         return lib().rso_blas_dot(len(a), _pf(a), _pf(b))
+    if _cpu_threads > 1:
+        return lib().rsf_dot(len(a), _pf(a), _pf(b), _blas_threads)
     total, lo = 0.0, 0
     for w in widths:
         total = total + lib().rso_blas_dot(w, _pf(a[lo:lo + w]), _pf(b[lo:lo + w]))
@@ -242,7 +437,11 @@ def power_method_norm2(A, iters=100, seed=0):
         nt = norm(t)
         if nt == 0.0:
             return est
-        v = t / nt
+        if _cpu_threads > 1:
+            v = np.empty(len(t))
+            lib().rsf_scale_div(len(t), _pf(v), _pf(t), float(nt))
+        else:
+            v = t / nt
     return float(est)
 
 
@@ -307,14 +506,14 @@ class OraclePreconditioner:
         t = matvec_transpose(f.L2, v)
         t = sparse_lower_solve_transpose(f.L1, t, unit_diag=True)
         t = sparse_lower_solve(f.L1, t, unit_diag=True)
-        return v + matvec(f.L2, t)
+        return _add(v, matvec(f.L2, t))
 
     def _solve_s(self, u):
         """pc.py:158-163."""
         if self.s_mode == "dense":
             return dense_cholesky_solve(self.S_factor, u)
         if self.s_mode == "identity":
-            return np.array(u, dtype=np.float64, copy=True)
+            return _copy(u)
         return cg_fixed_steps(self.s_matvec_implicit, u, self.cg_iters)
 
     def apply(self, r1, r2):
@@ -324,9 +523,9 @@ class OraclePreconditioner:
         if r1.shape != (self.n,) or r2.shape != (self.split_rows,):
             raise ValueError("residual component lengths do not match the split")
         if self.split_rows:
-            u = r2 - self.y_apply(r1)
+            u = _sub(r2, self.y_apply(r1))
             w = self._solve_s(u)
-            y = r1 + self.y_apply_transpose(w)
+            y = _add(r1, self.y_apply_transpose(w))
         else:
             y = r1
         v = sparse_lower_solve(self.factors.L1, y, unit_diag=True)
@@ -336,23 +535,23 @@ class OraclePreconditioner:
 def cg_fixed_steps(op, u, iters):
     """pc.py:284-310."""
     w = np.zeros(len(u))
-    r = np.array(u, dtype=np.float64, copy=True)
+    r = _copy(u)
     rho = dot(r, r)
     if rho == 0.0:
         return w
-    p = r.copy()
+    p = _copy(r)
     for _ in range(iters):
         q = op(p)
         pq = dot(p, q)
         if pq <= 0.0:
             break
         alpha = rho / pq
-        w += alpha * p
-        r -= alpha * q
+        _axpy(w, alpha, p, +1)
+        _axpy(r, alpha, q, -1)
         rho_new = dot(r, r)
         if rho_new == 0.0:
             break
-        p = r + (rho_new / rho) * p
+        p = _xpby(r, rho_new / rho, p)
         rho = rho_new
     return w
 
@@ -382,10 +581,10 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
     n = int(A.ncols)
     b_norm = float(norm(b))
     if pre is not None:
-        perm = np.asarray(pre.factors.row_perm.perm)
+        perm = np.ascontiguousarray(pre.factors.row_perm.perm, dtype=np.int64)
 
         def precondition(r):
-            rp = r[perm]
+            rp = _gather(r, perm)
             return pre.apply(rp[:n], rp[n:])
 
         psize, nmod = pre.psize, pre.factors.nmod
@@ -405,7 +604,7 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
         }
 
     x = np.zeros(n)
-    r = b.copy()
+    r = _copy(b)
     z = matvec_transpose(A, r)
     alphas, sigmas, x_norms, history = [], [], [0.0], []
     converged = False
@@ -416,12 +615,12 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
 
     h = precondition(r)
     rho = float(dot(z, h))
-    p = h.copy()
+    p = _copy(h)
     stopped_early = False
     for it in range(max_iters):
         sigma = rho if rho > 0.0 else float(dot(z, p))
         if sigma == 0.0:
-            p = z.copy()
+            p = _copy(z)
             sigma = float(dot(z, z))
             rho = sigma
         q = matvec(A, p)
@@ -430,8 +629,8 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
             stopped_early = True
             break
         alpha = sigma / qq
-        x += alpha * p
-        r -= alpha * q
+        _axpy(x, alpha, p, +1)
+        _axpy(r, alpha, q, -1)
         alphas.append(alpha)
         sigmas.append(sigma)
         x_norms.append(float(norm(x)))
@@ -453,7 +652,7 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
             break
         h = precondition(r)
         rho_new = float(dot(z, h))
-        p = h + (rho_new / rho) * p if rho != 0.0 else h.copy()
+        p = _xpby(h, rho_new / rho, p) if rho != 0.0 else _copy(h)
         rho = rho_new
 
     if stopped_early and not converged:
@@ -467,6 +666,83 @@ def pcgls(A, b, pre, norm_A, delta=1e-10, max_iters=2000, d=5, ratio_raw=False,
                 break
 
     its = its_certified if converged else iters_run
-    fr = b - matvec(A, x)
+    fr = _sub(b, matvec(A, x))
     return x, report(its, converged, stopped_early and not converged, history,
                      float(norm(fr)), float(norm(matvec_transpose(A, fr))))
+
+
+# ---------------------------------------------------------------------------
+# host setup (reference arm of bench.py: sets the configs up with no product
+# code) -- column_scale sc.py:405-425, ilup_factorize il.py:211-368
+# ---------------------------------------------------------------------------
+
+
+class Csc:
+    """Minimal CscMatrix (sc.py:27-131 fields): int64 col_ptr/row_idx, f64 values."""
+
+    def __init__(self, nrows, ncols, col_ptr, row_idx, values):
+        self.nrows, self.ncols = int(nrows), int(ncols)
+        self.col_ptr, self.row_idx, self.values = col_ptr, row_idx, values
+
+    @property
+    def nnz(self):
+        return int(self.col_ptr[-1])
+
+    def column_counts(self):
+        return np.diff(self.col_ptr)
+
+
+class _Perm:
+    def __init__(self, perm):
+        self.perm = perm
+
+
+class Factors:
+    """IlupFactors fields (il.py:53-77)."""
+
+    def __init__(self, perm, L1, L2, U, nmod, row_counts):
+        self.row_perm, self.L1, self.L2, self.U = _Perm(perm), L1, L2, U
+        self.nmod, self.row_counts_final = nmod, row_counts
+
+
+def column_scale(A):
+    """sc.py:405-425 with numpy's own reduceat / sqrt / divide (the same
+    calls the reference makes).  Returns (scaled Csc, norms)."""
+    counts = np.diff(A.col_ptr)
+    empty = np.flatnonzero(counts == 0)
+    if len(empty):
+        raise ValueError(f"cannot scale zero column {empty[0]}")
+    sq = np.zeros(A.ncols)
+    sq[:] = np.add.reduceat(A.values * A.values, A.col_ptr[:-1])
+    norms = np.sqrt(sq)
+    S = Csc(A.nrows, A.ncols, A.col_ptr.copy(), A.row_idx.copy(), A.values / np.repeat(norms, counts))
+    return S, norms
+
+
+def ilup_factorize(A, p=10, tau=0.0, mu=0.1, small=1e-10):
+    """il.py:211-368 (oracle/ilupref.c).  Returns Factors."""
+    m, n, cp, ri, va = _csc(A)
+    h = ctypes.c_void_p()
+    err = ctypes.c_int64(-1)
+    rc = lib().orc_ilup_factorize(m, n, _p64(cp), _p64(ri), _pf(va), int(p), float(tau), float(mu),
+                                  float(small), ctypes.byref(h), ctypes.byref(err))
+    if rc == 1:
+        raise ValueError("invalid ILUP input or parameters")
+    if rc == 2:
+        raise np.linalg.LinAlgError(f"non-finite value in column {err.value} of the factorization")
+    if rc != 0:
+        raise MemoryError("oracle ILUP: out of memory")
+    try:
+        n1, n2, nu, nm = (ctypes.c_int64() for _ in range(4))
+        lib().orc_ilup_sizes(h, ctypes.byref(n1), ctypes.byref(n2), ctypes.byref(nu), ctypes.byref(nm))
+        perm, rcnt = np.empty(m, dtype=np.int64), np.empty(m, dtype=np.int64)
+        l1p, l2p, up = (np.empty(n + 1, dtype=np.int64) for _ in range(3))
+        l1i, l1v = np.empty(n1.value, dtype=np.int64), np.empty(n1.value)
+        l2i, l2v = np.empty(n2.value, dtype=np.int64), np.empty(n2.value)
+        ui, uv = np.empty(nu.value, dtype=np.int64), np.empty(nu.value)
+        lib().orc_ilup_copy(h, _p64(perm), _p64(rcnt), _p64(l1p), _p64(l1i), _pf(l1v), _p64(l2p), _p64(l2i),
+                            _pf(l2v), _p64(up), _p64(ui), _pf(uv))
+    finally:
+        lib().orc_ilup_free(h)
+    return Factors(perm, Csc(n, n, l1p, l1i, l1v), Csc(m - n, n, l2p, l2i, l2v), Csc(n, n, up, ui, uv),
+                   int(nm.value), rcnt)

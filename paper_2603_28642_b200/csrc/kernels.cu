@@ -114,31 +114,40 @@ __device__ __forceinline__ void dot_chunk(int64_t n, int T, int t, int64_t &lo, 
 }
 
 // lane 0 of every block: publish this chunk's result; the last block to
-// finish sums the partials in chunk order and writes the dot
-__device__ __forceinline__ void dot_combine(double d, double *out, int sqrt_out, const DotChunks &c) {
+// finish sums the partials in chunk order and writes the dot.  A gated block
+// (skip) still counts itself, so the slot's counter is back at 0 after every
+// launch even when the gate flips while the launch is being dispatched (the
+// estimator on the side branch can stop the solve mid-launch); the value is
+// then not written -- nothing downstream of a stop reads it.
+__device__ __forceinline__ void dot_combine(double d, double *out, int sqrt_out, const DotChunks &c, bool skip) {
     if (c.T <= 1) {
-        out[0] = sqrt_out ? sqrt(d) : d;
+        if (!skip) out[0] = sqrt_out ? sqrt(d) : d;
         return;
     }
-    c.part[blockIdx.x] = d;
+    if (!skip) c.part[blockIdx.x] = d;
     __threadfence();
-    const unsigned prev = atomicAdd(c.cnt, 1u);
-    if (prev != (unsigned)c.T - 1) return;
+    const unsigned prev = atomicAdd(c.cnt, skip ? 0x10000u + 1u : 1u);
+    if ((prev & 0xFFFFu) != (unsigned)c.T - 1) return;
     __threadfence();
+    *c.cnt = 0;  // ready for the next replay of the graph
+    if (skip || (prev >> 16)) return;  // some chunk was gated: no result
     double sum = 0.0;
     for (int i = 0; i < c.T; ++i) sum = __dadd_rn(sum, ((volatile const double *)c.part)[i]);
     out[0] = sqrt_out ? sqrt(sum) : sum;
-    *c.cnt = 0;  // ready for the next replay of the graph
 }
 
 __global__ void k_dot_exact(int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,
                             const int *need, DotChunks ch) {
-    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    // `need` is set before the launch; only the gate can flip during it
+    if (need && !*(volatile const int *)need) return;
+    const bool skip = __shfl_sync(0xffffffffu, gated(g) ? 1 : 0, 0) != 0;
     int64_t lo = 0, w = n;
     if (ch.T > 1) dot_chunk(n, ch.T, blockIdx.x, lo, w);
-    double d = warp_blas_dot(
-        w, [&](int64_t i) { return vin(a, lo + i); }, [&](int64_t i) { return vin(b, lo + i); });
-    if (threadIdx.x == 0) dot_combine(d, out, sqrt_out, ch);
+    double d = 0.0;
+    if (!skip)
+        d = warp_blas_dot(
+            w, [&](int64_t i) { return vin(a, lo + i); }, [&](int64_t i) { return vin(b, lo + i); });
+    if (threadIdx.x == 0) dot_combine(d, out, sqrt_out, ch, skip);
 }
 
 // Fixed-shape two-level tree (RSB_DOT_TREE): block b sums a fixed chunk in a
@@ -612,7 +621,11 @@ __device__ __forceinline__ double canonical(double v) {
 __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const double *a_all, const double *b_all,
                                                          double *out, int sqrt_out, Gate g, const int *need,
                                                          DotChunks ch) {
-    if (gated(g) || (need && !*(volatile const int *)need)) return;
+    if (need && !*(volatile const int *)need) return;
+    if (__shfl_sync(0xffffffffu, gated(g) ? 1 : 0, 0)) {  // still count this chunk (dot_combine)
+        if (threadIdx.x == 0) dot_combine(0.0, out, sqrt_out, ch, true);
+        return;
+    }
     extern __shared__ __align__(16) double dbuf[];
     constexpr int kBuf = kDotChunk + 2;  // one stage of one operand: a chunk shifted by <= 1 element
     unsigned long long *bar = reinterpret_cast<unsigned long long *>(dbuf + kDotStages * 2 * kBuf);
@@ -706,7 +719,7 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
         if (lane == 0 && c + kDotStages < nch) issue(c + kDotStages);
     }
     const double d = warp_blas_finish(acc, n, [&](int64_t i) { return a[i]; }, [&](int64_t i) { return b[i]; });
-    if (lane == 0) dot_combine(d, out, sqrt_out, ch);
+    if (lane == 0) dot_combine(d, out, sqrt_out, ch, false);
 }
 
 // right-hand side in task-position order: bpos[t] = a(row_t) [+ c[row_t]]
@@ -1315,10 +1328,15 @@ int launch_xpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, co
 }
 
 int prepare_chol(int64_t s) {
+    // grow-only, like prepare_trsv_cta: a smaller s must not shrink the limit
+    // an earlier (larger) preconditioner's launches rely on
+    static size_t granted = 48 * 1024;
     const size_t smem = (size_t)s * sizeof(double);
-    if (smem > 48 * 1024 && smem <= 200 * 1024)
+    if (smem > granted && smem <= 200 * 1024) {
         RSB_TRY_CUDA(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
+        granted = smem;
+    }
     return RSB_OK;
 }
 

@@ -143,20 +143,28 @@ def config3(seed=3, n=1_000_000, m=None, k=8):
     return A, b
 
 
-def config4(seed=4, n=8_000_000, m=None, nrhs=64):
+def config4(seed=4, n=8_000_000, m=None, nrhs=64, first_rhs=0):
     """Multi-GPU scale problem: as config 0 with 6 nnz/row -- rows 0..n-1
     diagonal + 5 off-diagonals, rows n..m-1 six N(0,1) entries, m = 2n; rows
-    permuted; nrhs right-hand sides N(0,1)^m drawn in order.
+    permuted; right-hand sides N(0,1)^m drawn in order.  Returns the rhs
+    j = first_rhs .. first_rhs + nrhs - 1 of that sequence (the earlier
+    ones are drawn and discarded), so a rank's shard of the 64-RHS batch is
+    the same vectors whichever rank draws it.
 
     Draws: _stacked_random_rows(k_top_off=5, k_bottom=6), permutation(m),
-    then rhs j = 0..nrhs-1 each standard_normal(m).
+    then rhs j = 0, 1, ... each standard_normal(m).
     """
     rng = np.random.default_rng(seed)
     m = 2 * n if m is None else m
     r, c, v = _stacked_random_rows(rng, m, n, 5, 6)
     perm = rng.permutation(m)
     A = CscMatrix.from_coo(m, n, perm[r], c, v)
-    B = np.stack([rng.standard_normal(m) for _ in range(nrhs)]) if nrhs else np.zeros((0, m))
+    del r, c, v, perm
+    for _ in range(first_rhs):
+        rng.standard_normal(m)
+    B = np.empty((nrhs, m))
+    for j in range(nrhs):
+        B[j] = rng.standard_normal(m)
     return A, B
 
 

@@ -157,3 +157,14 @@ def test_inner_cg_step_counts_bitwise(k):
     # and the next application runs all k steps again
     r1b, r2b = rng.standard_normal(400), rng.standard_normal(200)
     assert np.array_equal(pre.apply(r1b, r2b), op.apply(r1b, r2b))
+
+
+def test_chol_smem_limit_is_grow_only():
+    """Two dense S solves whose vectors need > 48 KB of shared memory: the
+    larger one must still launch after the smaller one was prepared
+    (kernels.cu prepare_chol keeps the largest granted limit)."""
+    for s in (7000, 6200, 7000):
+        g = np.eye(s) * 2.0
+        b = np.arange(1.0, s + 1.0)
+        x = P.dense_cholesky_solve(P.DenseMatrix(g), b)
+        assert np.array_equal(x, b / 4.0)

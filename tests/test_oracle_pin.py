@@ -170,3 +170,104 @@ def test_oracle_live_against_reference():
         assert np.array_equal(O.sparse_lower_solve(low, b, True), rs.sparse_lower_solve(low, b, True))
         assert np.array_equal(O.sparse_lower_solve_transpose(low, b, True),
                               rs.sparse_lower_solve_transpose(low, b, True))
+
+
+# ---- host setup restatements and the threaded evaluation (bench.py's
+# reference arm uses these instead of any product code)
+
+
+def _same(a, b):
+    return (a.nrows, a.ncols) == (b.nrows, b.ncols) and np.array_equal(a.col_ptr, b.col_ptr) \
+        and np.array_equal(a.row_idx, b.row_idx) and np.array_equal(a.values, b.values)
+
+
+@pytest.mark.parametrize("name", ["cfg0s_mu0.1", "cfg0s_mu1.0", "cfg1s_mu1.0"])
+def test_oracle_setup_matches_reference_fixtures(name):
+    from paper_2603_28642_b200 import workloads as W
+
+    z = golden(f"{name}.npz")
+    prm = golden_json(f"{name}_reports.json")["params"]
+    A, _ = W.config0(seed=0, m=600, n=400) if name.startswith("cfg0") else W.config1(seed=1, g=24)
+    S, scale = O.column_scale(A)
+    assert _same(S, csc_from(z, "S")) and np.array_equal(scale, z["scale"])
+    f = O.ilup_factorize(S, **prm)
+    want = factors_from(z)
+    assert np.array_equal(f.row_perm.perm, want.row_perm.perm)
+    for k in ("L1", "L2", "U"):
+        assert _same(getattr(f, k), getattr(want, k)), k
+    assert f.nmod == want.nmod and np.array_equal(f.row_counts_final, want.row_counts_final)
+
+
+def test_oracle_ilup_config4_n1e5_matches_reference_hashes():
+    """Digests of the reference's own column_scale + ilup_factorize at the
+    config-4 structure, n = 1e5, mu = 1 (tests/golden/make_cfg4_hashes.py)."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_cfg4_hashes import factor_digests
+
+    from paper_2603_28642_b200 import workloads as W
+
+    want = golden_json("cfg4_factor_hashes.json")["100000"]
+    A, _ = W.config4(seed=4, n=100_000, nrhs=0)
+    S, scale = O.column_scale(A)
+    f = O.ilup_factorize(S, p=10, tau=0.0, mu=1.0)
+    got = factor_digests(S.values, scale, f)
+    for k, v in got.items():
+        assert v == want[k], k
+
+
+def test_oracle_ilup_random_vs_live_reference():
+    rs = reference()
+    rng = np.random.default_rng(5)
+    for t in range(30):
+        m = int(rng.integers(2, 60))
+        n = int(rng.integers(1, m + 1))
+        a = rng.standard_normal((m, n)) * (rng.random((m, n)) < rng.uniform(0.05, 1.0))
+        if t % 4 == 0 and n > 2:
+            a[:, 2 % n] = a[:, 0]
+        for j in range(n):
+            if not a[:, j].any():
+                a[rng.integers(0, m), j] = 1.0
+        prm = dict(p=int(rng.integers(1, 12)), tau=float(rng.choice([0.0, 1e-2, 0.3])),
+                   mu=float(rng.choice([0.1, 0.5, 1.0])))
+        A = rs.CscMatrix.from_dense(a)
+        fr = rs.ilup_factorize(A, rs.IlupParams(**prm))
+        fo = O.ilup_factorize(A, **prm)
+        assert np.array_equal(fr.row_perm.perm, fo.row_perm.perm), t
+        for k in ("L1", "L2", "U"):
+            assert _same(getattr(fr, k), getattr(fo, k)), (t, k)
+        assert fr.nmod == fo.nmod and np.array_equal(fr.row_counts_final, fo.row_counts_final)
+
+
+def test_fast_kernels_match_sequential():
+    """rsfast.c (threaded, level-scheduled, CSR) gives the sequential
+    restatement's bits: kernels, the T-thread dot, a whole pcgls run."""
+    from paper_2603_28642_b200 import workloads as W
+
+    A, B = W.config4(seed=4, n=20_000, nrhs=1)
+    S, _ = O.column_scale(A)
+    f = O.ilup_factorize(S, p=10, tau=0.0, mu=1.0)
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal(S.ncols), rng.standard_normal(S.nrows)
+    prev_bt = O.set_blas_threads(8)
+    try:
+        seq = [O.matvec(S, x), O.matvec_transpose(S, y), O.sparse_lower_solve(f.L1, x, unit_diag=True),
+               O.sparse_upper_solve(f.U, x), O.sparse_lower_solve_transpose(f.L1, x, unit_diag=True),
+               O.dot(y, y), O.power_method_norm2(S, 5, 4)]
+        pre = O.OraclePreconditioner(f, "cg", "implicit", 2)
+        xs, rs_ = O.pcgls(S, B[0], pre, seq[-1], delta=1e-300, max_iters=4)
+        prev = O.set_cpu_threads(4)
+        try:
+            fast = [O.matvec(S, x), O.matvec_transpose(S, y), O.sparse_lower_solve(f.L1, x, unit_diag=True),
+                    O.sparse_upper_solve(f.U, x), O.sparse_lower_solve_transpose(f.L1, x, unit_diag=True),
+                    O.dot(y, y), O.power_method_norm2(S, 5, 4)]
+            xf, rf = O.pcgls(S, B[0], pre, seq[-1], delta=1e-300, max_iters=4)
+        finally:
+            O.set_cpu_threads(prev)
+            O.clear_prep_cache()
+    finally:
+        O.set_blas_threads(prev_bt)
+    for k, (a, b) in enumerate(zip(seq, fast)):
+        assert np.array_equal(a, b), k
+    assert np.array_equal(xs, xf) and rs_ == rf
