@@ -74,6 +74,7 @@ typedef struct rsb_mat rsb_mat;
 typedef struct rsb_pre rsb_pre;
 typedef struct rsb_solver rsb_solver;
 typedef struct rsb_ilup rsb_ilup;
+typedef struct rsb_bsolver rsb_bsolver;
 
 /* ---- library / context ------------------------------------------------ */
 const char *rsb_last_error(void);
@@ -128,7 +129,8 @@ int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
 #define RSB_TRSV_STAGED 1
 #define RSB_TRSV_LEAN 2
 #define RSB_TRSV_LEVELS 3
-#define RSB_TRSV_LSYNC 4 /* persistent level-synchronous grid solve (wide, shallow DAGs; default there) */
+#define RSB_TRSV_LSYNC 4 /* persistent level-synchronous grid solve, items taken in level order (option) */
+#define RSB_TRSV_LEVELSYNC 5 /* cooperative grid solve walking the levels with grid barriers (wide DAGs; default) */
 int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n);
 /* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),
  * drawn by the caller (host RNG stays on the host). */
@@ -214,6 +216,28 @@ int rsb_pcgls(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg *cfg
 int rsb_pcgls_many(int count, rsb_solver *const *S, const double *const *b, int where,
                    const rsb_cgls_cfg *cfg, double *const *x, rsb_report *reps, double *history,
                    int64_t history_cap);
+
+/* ---- batched solve: up to 8 right-hand sides sharing A and pre ---------- */
+/* config 4's 64 RHS run 8 per GPU with replicated factors.
+ * The reference solves one b per pcgls call (sv.py:120-126); a batch solver
+ * advances 1..8 of those solves together through kernels that read every
+ * matrix and factor entry once for all of them (RHS-interleaved vectors).
+ * Each RHS's x and report equal rsb_pcgls on that b, bit for bit.  Needs
+ * the implicit Y with cg or identity coupling (or pre == NULL) and wide
+ * (grid-schedule) triangular solves; EINVAL otherwise. */
+int rsb_bsolver_create(rsb_mat *A, rsb_pre *pre, rsb_bsolver **out);
+int rsb_bsolver_destroy(rsb_bsolver *S);
+/* B: k x m row-major (host or device per `where`), 1 <= k <= 8; status[k] */
+int rsb_bsolver_start(rsb_bsolver *S, int k, const double *B, int where, const rsb_cgls_cfg *cfg, int *status);
+int rsb_bsolver_iterate(rsb_bsolver *S, int64_t kit, int *all_done);
+/* X: k x n row-major; reps[k]; history[r * history_cap ...] */
+int rsb_bsolver_finish(rsb_bsolver *S, double *X, int where, rsb_report *reps, double *history,
+                       int64_t history_cap);
+int rsb_pcgls_batch8(rsb_bsolver *S, int k, const double *B, int where, const rsb_cgls_cfg *cfg, double *X,
+                     rsb_report *reps, double *history, int64_t history_cap);
+/* measurement, as rsb_solver_bench, for the whole batch */
+int rsb_bsolver_bench(rsb_bsolver *S, int64_t kit, int flush, double *iter_ms, double *tri_ms,
+                      int64_t *tri_launches, int64_t *kernels_per_iter, int *all_done);
 
 /* ---- host setup (stays on the CPU; timed separately) -------------------- */
 /* ilup_factorize (il.py:211-368), bit-identical factors.  Inputs: scaled A

@@ -91,6 +91,14 @@ _SIGS = {
                        ctypes.POINTER(vp), ctypes.POINTER(ReportC), vp, i64],
     "rsb_solver_bench": [vp, i64, ctypes.c_int, f64p, f64p, i64p, i64p, ctypes.POINTER(ctypes.c_int)],
     "rsb_l2_flush": [vp],
+    "rsb_bsolver_create": [vp, vp, ctypes.POINTER(vp)],
+    "rsb_bsolver_destroy": [vp],
+    "rsb_bsolver_start": [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.POINTER(CglsCfgC), ctypes.POINTER(ctypes.c_int)],
+    "rsb_bsolver_iterate": [vp, i64, ctypes.POINTER(ctypes.c_int)],
+    "rsb_bsolver_finish": [vp, vp, ctypes.c_int, ctypes.POINTER(ReportC), vp, i64],
+    "rsb_pcgls_batch8": [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.POINTER(CglsCfgC), vp, ctypes.POINTER(ReportC),
+                         vp, i64],
+    "rsb_bsolver_bench": [vp, i64, ctypes.c_int, f64p, f64p, i64p, i64p, ctypes.POINTER(ctypes.c_int)],
     "rsb_ilup_factorize": [i64, i64, vp, vp, vp, i64, f64, f64, f64, ctypes.POINTER(vp)],
     "rsb_ilup_sizes": [vp, i64p, i64p, i64p, i64p],
     "rsb_ilup_copy": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],

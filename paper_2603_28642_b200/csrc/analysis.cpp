@@ -454,6 +454,9 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         // DAGs of at most kLsMaxLevels levels
         S->lsync = S->wide && nlev <= kLsMaxLevels && gv && std::strcmp(gv, "lsync") == 0;
         if (S->lsync) S->level_launch = false;
+        // wide schedules walk their levels in one cooperative kernel unless
+        // the sync-free kernel is requested (RSB_TRSV_GRID=syncfree)
+        S->level_sync = S->wide && !S->lsync && !S->level_launch && !(gv && std::strcmp(gv, "syncfree") == 0);
     }
     std::vector<int32_t> ls_pos, ls_lev, ls_lit;
     if (S->lsync) {

@@ -417,7 +417,10 @@ int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n) {
     RSB_TRY(get_tri(T, kind, &S));
     *variant = S->lean_n ? RSB_TRSV_LEAN
                          : (S->single_cta ? RSB_TRSV_STAGED
-                                          : (S->level_launch ? RSB_TRSV_LEVELS : (S->lsync ? RSB_TRSV_LSYNC : RSB_TRSV_GRID)));
+                                          : (S->level_launch ? RSB_TRSV_LEVELS
+                                                             : (S->lsync ? RSB_TRSV_LSYNC
+                                                                         : (S->level_sync ? RSB_TRSV_LEVELSYNC
+                                                                                          : RSB_TRSV_GRID))));
     *lean_n = S->lean_n;
     return RSB_OK;
 }

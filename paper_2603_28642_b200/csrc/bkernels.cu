@@ -1,0 +1,607 @@
+// Kernels of the batched solve: kBatch = 8 right-hand sides that share A and
+// the preconditioner (config 4: 8 RHS per GPU).
+//
+// Vectors are RHS-interleaved, v[i * 8 + r], so one matrix or factor entry
+// is read once and applied to 8 independent chains, and every gathered
+// operand is one 64-byte row instead of an 8-byte piece of a 32-byte
+// sector.  Per right-hand side the arithmetic is exactly the single-RHS
+// kernels' (the reference's order), so every RHS of the batch is bit-
+// identical to its own pcgls run.
+//
+// Heavy kernels (products, solves, dots) compute all 8 right-hand sides
+// unconditionally -- a stopped RHS's scratch vectors are never read again --
+// and skip only when the whole batch has stopped; the updates of persistent
+// state (x, r, p, w of the inner CG) are gated per RHS.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "bsolver.cuh"
+#include "device_common.cuh"
+
+namespace rsb {
+
+namespace {
+
+constexpr int kB = kBatch;
+constexpr int kBlk = 256;
+
+__device__ __forceinline__ int64_t bidx(const VecIn &v, int64_t i) {
+    return v.g ? (int64_t)v.g[i + v.off] : i + v.off;
+}
+__device__ __forceinline__ bool all_off(const int *all_done) {
+    return all_done && *(volatile const int *)all_done != 0;
+}
+__device__ __forceinline__ bool rhs_off(const BGate &g, int r) {
+    return (g.a && *(volatile const int *)((const char *)g.a + (size_t)r * g.sa)) ||
+           (g.b && *(volatile const int *)((const char *)g.b + (size_t)r * g.sb));
+}
+__device__ __forceinline__ const double *bscal(const double *p, int stride, int r) {
+    return (const double *)((const char *)p + (size_t)r * stride);
+}
+
+inline int grid_for_lines(int64_t lines) {  // an octet of lanes per line
+    return (int)std::max<int64_t>(1, (lines * kB + kBlk - 1) / kBlk);
+}
+inline int grid_stride_n(int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlk - 1) / kBlk, 148 * 32));
+}
+
+// ---- y = A x (CSR, row-sequential from 0.0; sc.py:212-221), octet per row
+template <int EPI>
+__global__ void __launch_bounds__(kBlk) kb_spmv(Compressed A, VecIn x, double *y, VecIn e, const int *all_done) {
+    if (all_off(all_done)) return;
+    const int64_t tid = blockIdx.x * (int64_t)kBlk + threadIdx.x;
+    const int64_t i = tid >> 3;
+    const int r = (int)(tid & 7);
+    if (i >= A.nlines) return;
+    const int lo = A.ptr[i], hi = A.ptr[i + 1];
+    double acc = 0.0;
+    int k = lo;
+    for (; k + 4 <= hi; k += 4) {  // the four gathers in flight together
+        int c[4];
+        double v[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            c[u] = A.idx[k + u];
+            v[u] = A.val[k + u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = x.p[bidx(x, c[u]) * kB + r];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    for (; k < hi; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], x.p[bidx(x, A.idx[k]) * kB + r]));
+    if (EPI == EPI_ADD) acc = __dadd_rn(e.p[bidx(e, i) * kB + r], acc);
+    if (EPI == EPI_SUB_FROM) acc = __dsub_rn(e.p[bidx(e, i) * kB + r], acc);
+    y[i * kB + r] = acc;
+}
+
+// ---- z = A^T y (CSC, z_j = p0 + pairwise(p1..); sc.py:224-235), octet per column
+struct BProd {
+    const double *val;
+    const int32_t *idx;
+    const VecIn *y;
+    int r;
+    __device__ double operator()(int64_t k) const { return __dmul_rn(val[k], y->p[bidx(*y, idx[k]) * kB + r]); }
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlk) kb_spmv_t(Compressed A, VecIn y, double *z, VecIn e, const int *all_done) {
+    if (all_off(all_done)) return;
+    const int64_t tid = blockIdx.x * (int64_t)kBlk + threadIdx.x;
+    const int64_t j = tid >> 3;
+    const int r = (int)(tid & 7);
+    if (j >= A.nlines) return;
+    const int lo = A.ptr[j], n = A.ptr[j + 1] - lo;
+    double acc = 0.0;
+    if (n > 0) {
+        const BProd t{A.val + lo, A.idx + lo, &y, r};
+        const double p0 = t(0);
+        const double rest = n - 1 <= 128 ? pw_leaf(t, 1, n - 1) : Pairwise<25, BProd>::sum(t, 1, n - 1);
+        acc = __dadd_rn(p0, rest);
+    }
+    if (EPI == EPI_ADD) acc = __dadd_rn(e.p[bidx(e, j) * kB + r], acc);
+    z[j * kB + r] = acc;
+}
+
+// ---- a @ b per RHS in the context's OpenBLAS order: block = 8 warps (warp
+// r = RHS r), grid = T chunks; partials combined by the last block in chunk
+// order (every block counts itself, so the slot is reset even when the
+// batch stops mid-launch)
+__global__ void __launch_bounds__(kBlk) kb_dot(int64_t n, VecIn a, VecIn b, double *out, int ostride, int sqrt_out,
+                                                 const int *all_done, BDotChunks ch) {
+    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ int s_skip;
+    if (threadIdx.x == 0) s_skip = all_off(all_done) ? 1 : 0;
+    __syncthreads();
+    const bool skip = s_skip != 0;
+    int64_t lo = 0, w = n;
+    if (ch.T > 1) {
+        int64_t rem = n;
+        for (int i = 0; i < (int)blockIdx.x; ++i) {
+            const int64_t wi = (rem + (ch.T - i) - 1) / (ch.T - i);
+            lo += wi;
+            rem -= wi;
+        }
+        w = (rem + (ch.T - (int)blockIdx.x) - 1) / (ch.T - (int)blockIdx.x);
+    }
+    double d = 0.0;
+    if (!skip)
+        d = warp_blas_dot(
+            w, [&](int64_t i) { return a.p[bidx(a, lo + i) * kB + r]; },
+            [&](int64_t i) { return b.p[bidx(b, lo + i) * kB + r]; });
+    double *o = (double *)((char *)out + (size_t)r * ostride);
+    if (ch.T <= 1) {
+        if (!skip && lane == 0) *o = sqrt_out ? sqrt(d) : d;
+        return;
+    }
+    if (!skip && lane == 0) ch.part[blockIdx.x * kB + r] = d;
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(ch.cnt, skip ? 0x10000u + 1u : 1u);
+        last = (prev & 0xFFFFu) == (unsigned)ch.T - 1;
+        if (last) {
+            __threadfence();
+            *ch.cnt = 0;
+            if (skip || (prev >> 16)) last = false;
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    if (lane == 0) {
+        double sum = 0.0;
+        for (int i = 0; i < ch.T; ++i) sum = __dadd_rn(sum, ((volatile const double *)ch.part)[i * kB + r]);
+        *o = sqrt_out ? sqrt(sum) : sum;
+    }
+}
+
+// ---- elementwise, per-RHS scalars and gates
+template <int SIGN>
+__global__ void kb_axpy(double *y, const double *x, const double *scal, int sstride, int64_t n, BGate g) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * kB; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i & 7);
+        if (rhs_off(g, r)) continue;
+        const double t = __dmul_rn(*bscal(scal, sstride, r), x[i]);
+        y[i] = SIGN > 0 ? __dadd_rn(y[i], t) : __dsub_rn(y[i], t);
+    }
+}
+
+// p = h + beta*p, or p = h where copy flag set (per RHS)
+__global__ void kb_xpby(double *p, const double *h, const double *beta, int bstride, const int *copy_flag,
+                        int cstride, int64_t n, BGate g) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * kB; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i & 7);
+        if (rhs_off(g, r)) continue;
+        const bool cp = copy_flag && *(const int *)((const char *)copy_flag + (size_t)r * cstride);
+        p[i] = cp ? h[i] : __dadd_rn(h[i], __dmul_rn(*bscal(beta, bstride, r), p[i]));
+    }
+}
+
+__global__ void kb_copy(double *dst, VecIn src, int64_t n, BGate g) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * kB; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i & 7);
+        if (rhs_off(g, r)) continue;
+        dst[i] = src.p[bidx(src, i >> 3) * kB + r];
+    }
+}
+
+__global__ void kb_fill(double *x, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * kB; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+// w = 0, r = u, p = u (_cg_fixed_steps start, pc.py:291-293)
+__global__ void kb_cg_init(double *w, double *rr, double *p, const double *u, int64_t s, BGate g) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s * kB; i += (int64_t)gridDim.x * blockDim.x) {
+        if (rhs_off(g, (int)(i & 7))) continue;
+        w[i] = 0.0;
+        rr[i] = u[i];
+        p[i] = u[i];
+    }
+}
+
+// row-major k x len (host order) <-> interleaved len x 8; missing RHS are zero
+__global__ void kb_pack(double *dst, const double *src, int64_t len, int k) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len * kB; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i & 7);
+        dst[i] = r < k ? src[(size_t)r * len + (i >> 3)] : 0.0;
+    }
+}
+__global__ void kb_unpack(double *dst, const double *src, int64_t len, int k) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len * k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / len, j = i - r * len;
+        dst[i] = src[j * kB + r];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batched sync-free triangular solve (wide schedules).  A lane owns one task
+// for all 8 right-hand sides: its entries are loaded once; the dependencies
+// of one half (4 RHS) at a time are read as two 16-byte loads per entry.
+// Completion is a per-row flag holding the launch's epoch (written after the
+// row's 8 values, release), so no sentinel fill of the 8n outputs is needed;
+// the epoch is bumped by a one-thread kernel before every solve.
+// ---------------------------------------------------------------------------
+constexpr unsigned kBtMinBackoff = 32, kBtMaxBackoff = 256;
+
+__device__ __forceinline__ int ld_flag(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_flag_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// 4 consecutive doubles (16-byte aligned), through L2
+__device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
+    const double2 a = __ldcg(reinterpret_cast<const double2 *>(p));
+    const double2 b = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+}
+
+// entries of the task past `from` (contiguous, then -1 padding)
+__device__ __noinline__ int bt_tail_len(const TriDev &T, int64_t base, int from, int K) {
+    int len = from;
+    for (int q = from; q < K; ++q) {
+        if (T.ecol[base + (int64_t)q * 32] < 0) break;
+        ++len;
+    }
+    return len;
+}
+
+__device__ __noinline__ bool bt_tail_ready(const TriDev &T, int64_t base, int from, int len, const int *flag, int E) {
+    for (int q0 = from; q0 < len; q0 += 8) {
+        int f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int c = q0 + u < len ? T.ecol[base + (int64_t)(q0 + u) * 32] : -1;
+            f[u] = c >= 0 ? ld_flag(flag + c) : E;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (f[u] != E) return false;
+    }
+    return true;
+}
+
+// entries past `from`, all published: continue the 4 chains of half h
+template <int MODE>
+__device__ __noinline__ void bt_tail(const TriDev &T, int64_t base, int from, int len, int h, const double *x,
+                                     double (&acc)[4], double (&dot)[4]) {
+    for (int q0 = from; q0 < len; q0 += 4) {
+        int c[4];
+        double v[4], xv[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            c[u] = q0 + u < len ? T.ecol[base + (int64_t)(q0 + u) * 32] : -1;
+            v[u] = q0 + u < len ? T.eval[base + (int64_t)(q0 + u) * 32] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (c[u] >= 0)
+                ld4(x + (int64_t)c[u] * kB + 4 * h, xv[u]);
+            else
+                xv[u][0] = xv[u][1] = xv[u][2] = xv[u][3] = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (c[u] < 0) break;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (!(MODE & 1)) {
+                    if (xv[u][q] != 0.0) acc[q] = __dsub_rn(acc[q], __dmul_rn(v[u], xv[u][q]));
+                } else {
+                    dot[q] = fma(v[u], xv[u][q], dot[q]);
+                }
+            }
+        }
+    }
+}
+
+template <int MODE, int N, bool TAIL>
+__global__ void __launch_bounds__(kBlk, 2) kb_trsv(TriDev T, VecIn a, const double *c, double *x, int *flag,
+                                                    const unsigned *epoch, int first_slice, int nslices,
+                                                    const int *all_done) {
+    if (all_off(all_done)) return;
+    const int E = (int)*(volatile const unsigned *)epoch;
+    const int lane = threadIdx.x & 31;
+    const int ntickets = nslices - first_slice;
+    auto take = [&]() {
+        int s = 0;
+        if (lane == 0) s = (int)atomicAdd(T.ticket, 1ull);
+        return __shfl_sync(0xffffffffu, s, 0);
+    };
+    int j = take();
+    while (j < ntickets) {
+        const int s = first_slice + j;
+        const int t = s * 32 + lane;
+        const bool valid = t < T.n;
+        const int64_t base = T.slice_off[s] + lane;
+        const int K = (int)((T.slice_off[s + 1] - T.slice_off[s]) >> 5);
+        int row = -1, len = 0;
+        int cols[N];
+        double vals[N];
+        double d = 1.0;
+        int64_t ai = 0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            cols[q] = -1;
+            vals[q] = 0.0;
+        }
+        unsigned need = 0;
+        if (valid) {
+            row = T.task_row[t];
+            ai = a.g ? (int64_t)a.g[row + a.off] : (int64_t)row + a.off;
+#pragma unroll
+            for (int q = 0; q < N; ++q)
+                if (q < K) {
+                    cols[q] = T.ecol[base + (int64_t)q * 32];
+                    vals[q] = T.eval[base + (int64_t)q * 32];
+                }
+#pragma unroll
+            for (int q = 0; q < N; ++q)
+                if (cols[q] >= 0) {
+                    need |= 1u << q;
+                    ++len;
+                }
+            if (TAIL && len == N && K > N) len = bt_tail_len(T, base, N, K);
+            if (MODE & 2) d = T.diag[t];
+        }
+        bool done = !valid;
+        unsigned prev = ~0u, backoff = 0;
+        for (;;) {
+            if (!__any_sync(0xffffffffu, !done)) break;
+            const bool stalled = done || need == prev;
+            if (__all_sync(0xffffffffu, stalled) && backoff) __nanosleep(backoff);
+            backoff = backoff ? min(backoff * 2, kBtMaxBackoff) : kBtMinBackoff;
+            prev = need;
+            if (!done) {
+                int f[N];
+#pragma unroll
+                for (int q = 0; q < N; ++q) f[q] = ((need >> q) & 1u) ? ld_flag(flag + cols[q]) : E;
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (f[q] == E) need &= ~(1u << q);
+                if (need == 0 && (!TAIL || len <= N || bt_tail_ready(T, base, N, len, flag, E))) {
+                    __threadfence();  // acquire: the flags were seen, now the values
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double acc[4], dot[4] = {0.0, 0.0, 0.0, 0.0};
+                        ld4(a.p + ai * kB + 4 * h, acc);
+                        if (c) {
+                            double cv[4];
+                            ld4(c + (int64_t)row * kB + 4 * h, cv);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) acc[q] = __dadd_rn(acc[q], cv[q]);
+                        }
+                        double xv[N][4];
+#pragma unroll
+                        for (int e = 0; e < N; ++e) {
+                            if (cols[e] >= 0)
+                                ld4(x + (int64_t)cols[e] * kB + 4 * h, xv[e]);
+                            else
+                                xv[e][0] = xv[e][1] = xv[e][2] = xv[e][3] = 0.0;
+                        }
+#pragma unroll
+                        for (int e = 0; e < N; ++e) {
+                            if (e >= len) break;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (!(MODE & 1)) {
+                                    if (xv[e][q] != 0.0) acc[q] = __dsub_rn(acc[q], __dmul_rn(vals[e], xv[e][q]));
+                                } else {
+                                    dot[q] = fma(vals[e], xv[e][q], dot[q]);
+                                }
+                            }
+                        }
+                        if (TAIL && len > N) bt_tail<MODE>(T, base, N, len, h, x, acc, dot);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if ((MODE & 1) && len > 0) acc[q] = __dsub_rn(acc[q], dot[q]);
+                            if (MODE & 2) acc[q] = __ddiv_rn(acc[q], d);
+                        }
+                        double2 *o = reinterpret_cast<double2 *>(x + (int64_t)row * kB + 4 * h);
+                        __stcg(o, make_double2(acc[0], acc[1]));
+                        __stcg(o + 1, make_double2(acc[2], acc[3]));
+                    }
+                    st_flag_release(flag + row, E);
+                    done = true;
+                }
+            }
+            __syncwarp();
+        }
+        j = take();
+    }
+}
+
+// level 0 of a batched solve: no dependencies.  An octet of lanes per task
+// (lane r: RHS r); after the octet's 8 stores, its first lane publishes the
+// row's flag (the octet barrier orders the stores before the release).
+template <int MODE>
+__global__ void kb_trsv_level0(TriDev T, VecIn a, const double *c, double *x, int *flag, const unsigned *epoch,
+                               int32_t lvl1, const int *all_done) {
+    if (all_off(all_done)) return;
+    const int E = (int)*(volatile const unsigned *)epoch;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int r = (int)(gt & 7);
+    const unsigned octet = 0xFFu << (threadIdx.x & 24);
+    for (int64_t t = gt >> 3; t < lvl1; t += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+        const int row = T.task_row[t];
+        double v = a.p[bidx(a, row) * kB + r];
+        if (c) v = __dadd_rn(v, c[(int64_t)row * kB + r]);
+        if (MODE & 2) v = __ddiv_rn(v, T.diag[t]);
+        x[(int64_t)row * kB + r] = v;
+        __syncwarp(octet);
+        if (r == 0) {
+            __threadfence();
+            st_flag_release(flag + row, E);
+        }
+    }
+}
+
+__global__ void kb_bump(unsigned *epoch) { *epoch += 1u; }
+
+using BtKernel = void (*)(TriDev, VecIn, const double *, double *, int *, const unsigned *, int, int, const int *);
+
+template <int MODE>
+BtKernel bt_kernel(int n, bool tail) {
+    if (n <= 4) return tail ? kb_trsv<MODE, 4, true> : kb_trsv<MODE, 4, false>;
+    return tail ? kb_trsv<MODE, 8, true> : kb_trsv<MODE, 8, false>;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int bpost(rsb_ctx *ctx) {
+    ctx->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("kernel launch failed: %s", cudaGetErrorString(e));
+        return RSB_ECUDA;
+    }
+    return RSB_OK;
+}
+
+int launch_bspmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, const int *all_done) {
+    if (A.nlines == 0) return RSB_OK;
+    const int grid = grid_for_lines(A.nlines);
+    switch (epi) {
+        case EPI_ADD: kb_spmv<EPI_ADD><<<grid, kBlk, 0, ctx->stream>>>(A, x, y, e, all_done); break;
+        case EPI_SUB_FROM: kb_spmv<EPI_SUB_FROM><<<grid, kBlk, 0, ctx->stream>>>(A, x, y, e, all_done); break;
+        default: kb_spmv<EPI_STORE><<<grid, kBlk, 0, ctx->stream>>>(A, x, y, e, all_done); break;
+    }
+    return bpost(ctx);
+}
+
+int launch_bspmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, const int *all_done) {
+    if (At.nlines == 0) return RSB_OK;
+    const int grid = grid_for_lines(At.nlines);
+    if (epi == EPI_ADD)
+        kb_spmv_t<EPI_ADD><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+    else
+        kb_spmv_t<EPI_STORE><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+    return bpost(ctx);
+}
+
+int launch_bdot(rsb_ctx *ctx, BDotRing &ring, int64_t n, VecIn a, VecIn b, double *out, int ostride, int sqrt_out,
+                const int *all_done) {
+    const int T = (ctx->blas_threads > 1 && n > 10000) ? ctx->blas_threads : 1;
+    BDotChunks ch{T, nullptr, nullptr};
+    if (T > 1) {
+        const int slot = (int)(ring.next++ % kDotSlots);
+        ch.part = ring.part + (size_t)slot * kMaxBlasThreads * kB;
+        ch.cnt = ring.cnt + slot;
+    }
+    kb_dot<<<T, kBlk, 0, ctx->stream>>>(n, a, b, out, ostride, sqrt_out, all_done, ch);
+    return bpost(ctx);
+}
+
+int launch_baxpy(rsb_ctx *ctx, double *y, const double *x, const double *scal, int sstride, int sign, int64_t n,
+                 BGate g) {
+    if (sign > 0)
+        kb_axpy<1><<<grid_stride_n(n * kB), kBlk, 0, ctx->stream>>>(y, x, scal, sstride, n, g);
+    else
+        kb_axpy<-1><<<grid_stride_n(n * kB), kBlk, 0, ctx->stream>>>(y, x, scal, sstride, n, g);
+    return bpost(ctx);
+}
+
+int launch_bxpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, int bstride, const int *copy_flag,
+                 int cstride, int64_t n, BGate g) {
+    kb_xpby<<<grid_stride_n(n * kB), kBlk, 0, ctx->stream>>>(p, h, beta, bstride, copy_flag, cstride, n, g);
+    return bpost(ctx);
+}
+
+int launch_bcopy(rsb_ctx *ctx, double *dst, VecIn src, int64_t n, BGate g) {
+    kb_copy<<<grid_stride_n(n * kB), kBlk, 0, ctx->stream>>>(dst, src, n, g);
+    return bpost(ctx);
+}
+
+int launch_bfill(rsb_ctx *ctx, double *x, int64_t n, double v) {
+    kb_fill<<<grid_stride_n(n * kB), kBlk, 0, ctx->stream>>>(x, n, v);
+    return bpost(ctx);
+}
+
+int launch_bcg_init(rsb_ctx *ctx, double *w, double *r, double *p, const double *u, int64_t s, BGate g) {
+    kb_cg_init<<<grid_stride_n(s * kB), kBlk, 0, ctx->stream>>>(w, r, p, u, s, g);
+    return bpost(ctx);
+}
+
+int launch_bpack(rsb_ctx *ctx, double *dst, const double *src, int64_t len, int k) {
+    kb_pack<<<grid_stride_n(len * kB), kBlk, 0, ctx->stream>>>(dst, src, len, k);
+    return bpost(ctx);
+}
+
+int launch_bunpack(rsb_ctx *ctx, double *dst, const double *src, int64_t len, int k) {
+    kb_unpack<<<grid_stride_n(len * k), kBlk, 0, ctx->stream>>>(dst, src, len, k);
+    return bpost(ctx);
+}
+
+bool btrsv_supported(const TriSched &T) { return T.wide && T.max_task < (1 << 20); }
+
+int launch_btrsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, BTriWs &ws,
+                 const int *all_done) {
+    if (T.n == 0) return RSB_OK;
+    if (!btrsv_supported(T)) {
+        set_error("batched triangular solve needs a wide (grid) schedule");
+        return RSB_ESTATE;
+    }
+    const bool trace = ctx->tracing && ctx->trace_n + 2 <= 64;
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
+    TriDev v = T.view();
+    v.ticket = ws.ticket;
+    kb_bump<<<1, 1, 0, ctx->stream>>>(ws.epoch);
+    RSB_TRY(bpost(ctx));
+    RSB_TRY_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned long long), ctx->stream));
+    const int32_t lvl1 = T.h_level_ptr.size() > 1 ? T.h_level_ptr[1] : T.n;
+    if (lvl1 > 0) {
+        const int g0 = grid_stride_n((int64_t)lvl1 * kB);
+        switch (T.mode & 3) {
+            case 0: kb_trsv_level0<0><<<g0, kBlk, 0, ctx->stream>>>(v, a, c, x, ws.flag, ws.epoch, lvl1, all_done); break;
+            case 1: kb_trsv_level0<1><<<g0, kBlk, 0, ctx->stream>>>(v, a, c, x, ws.flag, ws.epoch, lvl1, all_done); break;
+            case 2: kb_trsv_level0<2><<<g0, kBlk, 0, ctx->stream>>>(v, a, c, x, ws.flag, ws.epoch, lvl1, all_done); break;
+            default: kb_trsv_level0<3><<<g0, kBlk, 0, ctx->stream>>>(v, a, c, x, ws.flag, ws.epoch, lvl1, all_done); break;
+        }
+        RSB_TRY(bpost(ctx));
+    }
+    const int nslices = (T.n + 31) / 32;
+    const int first_slice = lvl1 / 32;
+    if (first_slice < nslices) {
+        const int wn = T.wide_n <= 4 ? 4 : 8;
+        const bool tail = T.max_task > wn;
+        BtKernel k;
+        switch (T.mode & 3) {
+            case 0: k = bt_kernel<0>(wn, tail); break;
+            case 1: k = bt_kernel<1>(wn, tail); break;
+            case 2: k = bt_kernel<2>(wn, tail); break;
+            default: k = bt_kernel<3>(wn, tail); break;
+        }
+        static int occ_cache[4][2][2] = {};
+        int &occ = occ_cache[T.mode & 3][wn == 8][tail];
+        if (occ == 0) {
+            RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBlk, 0));
+            occ = std::max(occ, 1);
+        }
+        int sms = 0;
+        RSB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int grid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)sms * occ, ((int64_t)(nslices - first_slice) * 32 + kBlk - 1) / kBlk));
+        k<<<grid, kBlk, 0, ctx->stream>>>(v, a, c, x, ws.flag, ws.epoch, first_slice, nslices, all_done);
+        RSB_TRY(bpost(ctx));
+    }
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
+    return RSB_OK;
+}
+
+}  // namespace rsb

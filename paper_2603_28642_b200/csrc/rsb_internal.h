@@ -234,6 +234,9 @@ struct TriSched {
     bool wide = false;
     // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
     bool lsync = false;
+    // wide DAGs: one cooperative kernel walking the levels with grid barriers
+    // (trsv_ls.cu); false: the sync-free kernel (trsv_wide.cu)
+    bool level_sync = false;
     int32_t ls_nitems = 0;
     int32_t *ls_item_pos = nullptr, *ls_item_level = nullptr, *ls_level_items = nullptr;
     unsigned *ls_cnt = nullptr;  // the schedule's own counters (calls without a workspace)
@@ -351,6 +354,10 @@ int prepare_trsv_cta(int64_t n);
 int prepare_trsv_lean(int64_t smem_bytes);
 int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
 int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g);
+// level-synchronous cooperative solve of a wide schedule for nb = 1 or 8
+// interleaved right-hand sides (rstat: per-RHS status words, stride in ints)
+int launch_trsv_ls(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x,
+                   unsigned *bar, Gate g, int nb, const int *rstat, int rstride);
 int launch_trsv_lsync(rsb_ctx *ctx, const TriSched &T, const TriDev &v, unsigned *counters, VecIn a,
                       const double *c, double *x, Gate g);
 constexpr size_t kLsCounters = 32 + (size_t)kLsMaxLevels * kLsRep;

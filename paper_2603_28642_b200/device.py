@@ -190,7 +190,7 @@ class DeviceMatrix:
         """(kernel family, longest task of the lean kernel or 0) of a solve."""
         v, n = ctypes.c_int(), ctypes.c_int()
         L.check(L.lib().rsb_trsv_variant(self.h, kind, ctypes.byref(v), ctypes.byref(n)))
-        return ("grid", "staged", "lean", "levels", "lsync")[v.value], n.value
+        return ("grid", "staged", "lean", "levels", "lsync", "levelsync")[v.value], n.value
 
     def levels(self, kind: int):
         nl, mw = ctypes.c_int64(), ctypes.c_int64()
@@ -228,6 +228,7 @@ def device_matrix(A, ctx: Context | None = None) -> DeviceMatrix:
 
 
 def clear_caches():
+    _bsolver_cache.clear()
     _batch_cache.clear()
     _mat_cache.clear()
     _pre_cache.clear()
@@ -412,4 +413,67 @@ def device_solvers(dA: DeviceMatrix, dpre: DevicePreconditioner | None, k: int) 
     _batch_cache[key] = s
     while len(_batch_cache) > 4:
         _batch_cache.popitem(last=False)
+    return s
+
+
+BATCH = 8  # right-hand sides per batched solver (csrc/bsolver.cu kBatch)
+
+
+class DeviceBatchSolver:
+    """Up to BATCH pcgls solves advanced together (rsb_bsolver): matrix and
+    factor entries are read once for all of them."""
+
+    def __init__(self, dA: DeviceMatrix, dpre: DevicePreconditioner | None):
+        self.dA, self.dpre = dA, dpre
+        self.ctx = dA.ctx
+        h = ctypes.c_void_p()
+        L.check(L.lib().rsb_bsolver_create(dA.h, dpre.h if dpre is not None else None, ctypes.byref(h)))
+        self.h = h
+
+    def start(self, B, cfg: "L.CglsCfgC", where=L.RSB_HOST):
+        k = B.shape[0] if where == L.RSB_HOST else B[1]
+        st = (ctypes.c_int * BATCH)()
+        ptr = L.ptr(B) if where == L.RSB_HOST else B[0]
+        L.check(L.lib().rsb_bsolver_start(self.h, int(k), ptr, where, ctypes.byref(cfg), st))
+        return list(st)[:k]
+
+    def iterate(self, k):
+        done = ctypes.c_int()
+        L.check(L.lib().rsb_bsolver_iterate(self.h, int(k), ctypes.byref(done)))
+        return bool(done.value)
+
+    def finish(self, k, n, cap):
+        X = np.empty((k, n))
+        reps = (L.ReportC * k)()
+        hist = np.empty((k, max(1, cap)))
+        L.check(L.lib().rsb_bsolver_finish(self.h, L.ptr(X), L.RSB_HOST, reps, L.ptr(hist), hist.shape[1]))
+        return X, reps, hist
+
+    def __del__(self):
+        try:
+            if _alive(self):
+                L.lib().rsb_bsolver_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+_bsolver_cache: "collections.OrderedDict[tuple, object]" = collections.OrderedDict()
+
+
+def device_batch_solver(dA: DeviceMatrix, dpre: DevicePreconditioner | None):
+    """The cached batched solver of (dA, dpre), or None when the problem
+    does not fit the batched kernels (explicit Y / dense S, narrow DAGs)."""
+    key = (id(dA), id(dpre))
+    hit = _bsolver_cache.get(key)
+    if hit is not None and hit[0] is dA and hit[1] is dpre:
+        _bsolver_cache.move_to_end(key)
+        return hit[2]
+    try:
+        s = DeviceBatchSolver(dA, dpre)
+    except ValueError:
+        s = None
+    _bsolver_cache[key] = (dA, dpre, s)
+    while len(_bsolver_cache) > 2:
+        _bsolver_cache.popitem(last=False)
     return s

@@ -109,3 +109,64 @@ def ilup_factorize(A, params: IlupParams | None = None) -> IlupFactors:
         nmod=int(nmod.value),
         row_counts_final=rc,
     )
+
+
+# ---------------------------------------------------------------------------
+# on-disk factor cache (host setup is the slow part of a config-4 run: the
+# serial ILUP takes minutes at n = 8e6)
+# ---------------------------------------------------------------------------
+
+_FACTOR_FIELDS = ("perm", "L1_ptr", "L1_idx", "L1_val", "L2_ptr", "L2_idx", "L2_val", "U_ptr", "U_idx",
+                  "U_val", "row_counts")
+
+
+def _cache_key(A, params: IlupParams) -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(f"{int(A.nrows)}x{int(A.ncols)}|p={params.p}|tau={params.tau!r}|mu={params.mu!r}|"
+             f"small={params.small!r}|v2".encode())
+    for a in (A.col_ptr, A.row_idx, A.values):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:24]
+
+
+def ilup_factorize_cached(A, params: IlupParams | None = None, cache_dir: str | None = None) -> IlupFactors:
+    """ilup_factorize with an on-disk cache keyed by a digest of A and the
+    parameters (cache_dir, else $RSB_FACTOR_CACHE; no caching when neither is
+    set).  A hit returns the stored factors unchanged: the same bits the
+    factorization produces."""
+    import os
+
+    params = params or IlupParams()
+    cache_dir = cache_dir or os.environ.get("RSB_FACTOR_CACHE")
+    if not cache_dir:
+        return ilup_factorize(A, params)
+    d = os.path.join(cache_dir, "ilup_" + _cache_key(A, params))
+    m, n = int(A.nrows), int(A.ncols)
+    try:
+        z = {k: np.load(os.path.join(d, k + ".npy")) for k in _FACTOR_FIELDS}
+        meta = np.load(os.path.join(d, "meta.npy"))
+        return IlupFactors(
+            row_perm=Permutation.from_perm(z["perm"]),
+            L1=CscMatrix(n, n, z["L1_ptr"], z["L1_idx"], z["L1_val"]),
+            L2=CscMatrix(m - n, n, z["L2_ptr"], z["L2_idx"], z["L2_val"]),
+            U=CscMatrix(n, n, z["U_ptr"], z["U_idx"], z["U_val"]),
+            nmod=int(meta[0]), row_counts_final=z["row_counts"])
+    except (OSError, ValueError, KeyError):
+        pass
+    f = ilup_factorize(A, params)
+    tmp = d + f".tmp{os.getpid()}"
+    os.makedirs(tmp, exist_ok=True)
+    arrays = {"perm": f.row_perm.perm, "row_counts": f.row_counts_final}
+    for k in ("L1", "L2", "U"):
+        M = getattr(f, k)
+        arrays.update({f"{k}_ptr": M.col_ptr, f"{k}_idx": M.row_idx, f"{k}_val": M.values})
+    for k, v in arrays.items():
+        np.save(os.path.join(tmp, k + ".npy"), np.ascontiguousarray(v))
+    np.save(os.path.join(tmp, "meta.npy"), np.array([f.nmod], dtype=np.int64))
+    try:
+        os.replace(tmp, d)
+    except OSError:
+        pass
+    return f

@@ -13,12 +13,14 @@ are bit-identical to the reference's.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib as L
-from .device import DeviceSolver, device_matrix, device_preconditioner, device_solver, device_solvers
+from .device import (BATCH, DeviceSolver, device_batch_solver, device_matrix, device_preconditioner,
+                     device_solver, device_solvers)
 
 
 @dataclass
@@ -163,12 +165,14 @@ def pcgls_batch(A, B, pre, cfg: CglsConfig, streams: int | None = None):
 
     Not in the reference API: the reference solves one b per pcgls call; the
     result for each row of B is exactly pcgls(A, B[j], pre, cfg), bit for
-    bit.  Each solve has its own CUDA stream and workspace, `streams` of them
-    per library call (default: all), reading the one device copy of A and the
-    factors.  Inside a call the library iterates them all at once when the
-    triangular solves are single-CTA (narrow DAGs, one SM each) and one after
-    two at a time when they are grid-wide (each fills most of the GPU;
-    RSB_BATCH_CONC overrides).  Returns (X with rows x_j, [reports]).
+    bit.  When the triangular solves are wide (grid schedules) and the
+    coupling is cg / identity with the implicit Y, groups of 8 right-hand
+    sides run through the batched kernels (csrc/bsolver.cu: every matrix and
+    factor entry read once per group).  Otherwise -- or with `streams` given,
+    or RSB_BATCH=streams -- each solve has its own CUDA stream and workspace
+    over the one device copy of A and the factors, `streams` of them per
+    library call (default: all); single-CTA solves (narrow DAGs, one SM each)
+    then iterate all at once.  Returns (X with rows x_j, [reports]).
     """
     B = np.ascontiguousarray(np.atleast_2d(np.asarray(B, dtype=np.float64)))
     m, n = int(A.nrows), int(A.ncols)
@@ -180,9 +184,27 @@ def pcgls_batch(A, B, pre, cfg: CglsConfig, streams: int | None = None):
     reports: list[SolveReport] = []
     if k == 0:
         return X, reports
-    width = k if streams is None else max(1, min(int(streams), k))
     dA = device_matrix(A)
     dpre = device_preconditioner(pre, dA.ctx) if pre is not None else None
+    mode = os.environ.get("RSB_BATCH", "auto")
+    bs = device_batch_solver(dA, dpre) if (mode != "streams" and streams is None) else None
+    if bs is not None:
+        # kernels that serve 8 right-hand sides per pass (csrc/bsolver.cu)
+        ccfg = DeviceSolver.cfg_struct(cfg.norm_A, cfg.delta, cfg.max_iters, cfg.estimator_delay, cfg.ratio_raw)
+        cap = cfg.max_iters + cfg.estimator_delay + 2
+        for lo in range(0, k, BATCH):
+            c = min(BATCH, k - lo)
+            Bc = np.ascontiguousarray(B[lo:lo + c])
+            reps = (L.ReportC * c)()
+            hist = np.empty((c, cap))
+            Xc = np.empty((c, n))
+            L.check(L.lib().rsb_pcgls_batch8(bs.h, c, L.ptr(Bc), L.RSB_HOST, ctypes.byref(ccfg), L.ptr(Xc), reps,
+                                             L.ptr(hist), cap))
+            X[lo:lo + c] = Xc
+            for i in range(c):
+                reports.append(_report(reps[i], hist[i, : min(reps[i].history_len, cap)].copy(), psize, nmod))
+        return X, reports
+    width = k if streams is None else max(1, min(int(streams), k))
     solvers = device_solvers(dA, dpre, width)
     ccfg = DeviceSolver.cfg_struct(cfg.norm_A, cfg.delta, cfg.max_iters, cfg.estimator_delay, cfg.ratio_raw)
     cap = cfg.max_iters + cfg.estimator_delay + 2

@@ -123,8 +123,13 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
     assert check(M, L.TRI_LOWER_UNIT, b, monkeypatch)[0] in ("staged", "grid", "levels")
     W = leveled_lower([6000] * 5, 4, rng)
     bw = rng.standard_normal(W.ncols)
-    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
-    # the level-synchronous persistent kernel on the same DAG
+    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levelsync"
+    # the sync-free kernel on the same DAG
+    with monkeypatch.context() as m:
+        m.setenv("RSB_TRSV_GRID", "syncfree")
+        W0 = P.CscMatrix(W.nrows, W.ncols, W.col_ptr.copy(), W.row_idx.copy(), W.values.copy())
+        assert check(W0, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+    # the level-synchronous item kernel on the same DAG
     with monkeypatch.context() as m:
         m.setenv("RSB_TRSV_GRID", "lsync")
         W1 = P.CscMatrix(W.nrows, W.ncols, W.col_ptr.copy(), W.row_idx.copy(), W.values.copy())
@@ -136,7 +141,8 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
         assert check(W2, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levels"
 
 
-@pytest.mark.parametrize("grid", ["lsync", "syncfree", "syncfree-pairs", "syncfree-unsorted", "syncfree-n4"])
+@pytest.mark.parametrize("grid", ["levelsync", "levelsync-n4", "lsync", "syncfree", "syncfree-pairs",
+                                  "syncfree-unsorted", "syncfree-n4"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -145,6 +151,10 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     without blocking (a dependency may sit in another lane of the warp)."""
     if grid == "lsync":
         monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
+    if grid.startswith("syncfree"):
+        monkeypatch.setenv("RSB_TRSV_GRID", "syncfree")
+    if grid == "levelsync-n4":  # level-synchronous with 4 register entries: long tasks take the tail
+        monkeypatch.setenv("RSB_WIDE_N", "4")
     if grid == "syncfree-pairs":
         monkeypatch.setenv("RSB_WIDE_EARLY", "0")
     if grid == "syncfree-unsorted":
@@ -165,7 +175,8 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     U = transpose(M)
     for kind in (L.TRI_UPPER, L.TRI_UPPER_T):
         check(U, kind, b, monkeypatch)
-    assert variant(M, L.TRI_LOWER)[0] == ("lsync" if grid == "lsync" else "grid")
+    want = {"lsync": "lsync", "levelsync": "levelsync", "levelsync-n4": "levelsync"}.get(grid, "grid")
+    assert variant(M, L.TRI_LOWER)[0] == want
 
 
 def test_many_chunks_every_kind(monkeypatch):
