@@ -454,9 +454,11 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         // DAGs of at most kLsMaxLevels levels
         S->lsync = S->wide && nlev <= kLsMaxLevels && gv && std::strcmp(gv, "lsync") == 0;
         if (S->lsync) S->level_launch = false;
-        // wide schedules walk their levels in one cooperative kernel unless
-        // the sync-free kernel is requested (RSB_TRSV_GRID=syncfree)
-        S->level_sync = S->wide && !S->lsync && !S->level_launch && !(gv && std::strcmp(gv, "syncfree") == 0);
+        // the level-synchronous cooperative kernel (RSB_TRSV_GRID=levelsync):
+        // measured slower than the sync-free default on config 4 at n = 8e6
+        // (U 1.13 vs 0.77 ms: every level waits for its longest rows;
+        // profiles/trsv_sweep_r02.json)
+        S->level_sync = S->wide && !S->lsync && !S->level_launch && gv && std::strcmp(gv, "levelsync") == 0;
     }
     std::vector<int32_t> ls_pos, ls_lev, ls_lit;
     if (S->lsync) {

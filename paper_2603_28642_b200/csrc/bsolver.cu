@@ -73,8 +73,7 @@ __global__ void kbc_start_rho(CglsState *st, double *x_norms, int64_t xstride) {
 }
 __global__ void kbc_it_begin(CglsState *st) {  // sv.py:203
     const int r = threadIdx.x;
-    if (st[r].status) return;
-    st[r].need_zp = !(st[r].rho > 0.0);
+    st[r].need_zp = st[r].status ? 0 : !(st[r].rho > 0.0);
 }
 __global__ void kbc_it_sigma(CglsState *st) {  // sv.py:203-208
     const int r = threadIdx.x;
@@ -265,7 +264,8 @@ int b_iteration(rsb_bsolver *S) {
     const int64_t m = S->m, n = S->n;
     kbc_it_begin<<<1, kB, 0, ctx->stream>>>(st);
     RSB_TRY(cchk(ctx));
-    RSB_TRY(launch_bdot(ctx, S->ring, n, VecIn{S->z, nullptr, 0}, VecIn{S->p, nullptr, 0}, &st[0].zp, kSt, 0, ad));
+    RSB_TRY(launch_bdot(ctx, S->ring, n, VecIn{S->z, nullptr, 0}, VecIn{S->p, nullptr, 0}, &st[0].zp, kSt, 0, ad,
+                        &st[0].need_zp, kSt));
     kbc_it_sigma<<<1, kB, 0, ctx->stream>>>(st);
     RSB_TRY(cchk(ctx));
     // p = z.copy() where sigma fell back to z.z (skip_retry == 0)

@@ -40,8 +40,9 @@ struct BTriWs {
 
 int launch_bspmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, const int *all_done);
 int launch_bspmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, const int *all_done);
+// out[r * ostride bytes] = a_r . b_r; skipped when all of need[r * nstride] are 0
 int launch_bdot(rsb_ctx *ctx, BDotRing &ring, int64_t n, VecIn a, VecIn b, double *out, int ostride, int sqrt_out,
-                const int *all_done);
+                const int *all_done, const int *need = nullptr, int nstride = 0);
 int launch_baxpy(rsb_ctx *ctx, double *y, const double *x, const double *scal, int sstride, int sign, int64_t n,
                  BGate g);
 int launch_bxpby(rsb_ctx *ctx, double *p, const double *h, const double *beta, int bstride, const int *copy_flag,

@@ -65,7 +65,7 @@ def main():
         settings.append(("syncfree", "", ""))
     for fam, p, occ in settings:
         key = f"{fam}" + (f"_P{p}" if p else "") + (f"_occ{occ}" if occ else "")
-        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam == "syncfree" else ""
+        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam == "syncfree" else "levelsync"
         os.environ["RSB_LS_P"] = p or "4"
         if occ:
             os.environ["RSB_LS_OCC"] = occ
