@@ -39,7 +39,7 @@ def factors_from(z):
     from paper_2603_28642_b200.types import Permutation
 
     return IlupFactors(Permutation.from_perm(z["perm"]), csc_from(z, "L1"), csc_from(z, "L2"),
-                       csc_from(z, "U"), int(z["nmod"]), z["row_counts"])
+                       csc_from(z, "U"), int(np.asarray(z["nmod"]).reshape(-1)[0]), z["row_counts"])
 
 
 def reference():

@@ -123,12 +123,12 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
     assert check(M, L.TRI_LOWER_UNIT, b, monkeypatch)[0] in ("staged", "grid", "levels")
     W = leveled_lower([6000] * 5, 4, rng)
     bw = rng.standard_normal(W.ncols)
-    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levelsync"
-    # the sync-free kernel on the same DAG
+    assert check(W, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+    # the level-synchronous cooperative kernel on the same DAG
     with monkeypatch.context() as m:
-        m.setenv("RSB_TRSV_GRID", "syncfree")
+        m.setenv("RSB_TRSV_GRID", "levelsync")
         W0 = P.CscMatrix(W.nrows, W.ncols, W.col_ptr.copy(), W.row_idx.copy(), W.values.copy())
-        assert check(W0, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "grid"
+        assert check(W0, L.TRI_LOWER_UNIT, bw, monkeypatch)[0] == "levelsync"
     # the level-synchronous item kernel on the same DAG
     with monkeypatch.context() as m:
         m.setenv("RSB_TRSV_GRID", "lsync")
@@ -151,8 +151,8 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     without blocking (a dependency may sit in another lane of the warp)."""
     if grid == "lsync":
         monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
-    if grid.startswith("syncfree"):
-        monkeypatch.setenv("RSB_TRSV_GRID", "syncfree")
+    if grid.startswith("levelsync"):
+        monkeypatch.setenv("RSB_TRSV_GRID", "levelsync")
     if grid == "levelsync-n4":  # level-synchronous with 4 register entries: long tasks take the tail
         monkeypatch.setenv("RSB_WIDE_N", "4")
     if grid == "syncfree-pairs":
