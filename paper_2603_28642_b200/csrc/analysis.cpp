@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <chrono>
 #include <numeric>
 
 #include "rsb_internal.h"
@@ -37,6 +38,15 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         return RSB_ESTATE;
     }
     const int64_t n = T->ncols;
+    const bool dbg = getenv("RSB_DEBUG_ANALYSIS") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto phase = [&](const char *what) {
+        if (!dbg) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rsb] analysis kind=%d %s %.3f s\n", kind, what,
+                std::chrono::duration<double>(now - t_prev).count());
+        t_prev = now;
+    };
     const int64_t *ptr = T->h_ptr.data();
     const int64_t *idx = T->h_idx.data();
     const double *val = T->h_val.data();
@@ -80,6 +90,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         }
     }
 
+    phase("checks");
     // per-task entry lists in the reference's accumulation order
     std::vector<int64_t> tptr(n + 1, 0);
     std::vector<Entry> ent;
@@ -124,6 +135,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         }
     }
 
+    phase("entry lists");
     // dependency levels
     std::vector<int32_t> level(n, 0);
     if (forward) {
@@ -162,6 +174,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
             });
     }
 
+    phase("levels + order");
     // warp-interleaved packing: slice widths
     const int64_t nslices = (n + 31) / 32;
     std::vector<int64_t> soff(nslices + 1, 0);
@@ -267,6 +280,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         }
     }
 
+    phase("slices + staged layout");
     std::vector<int32_t> ecol(slots, -1);
     std::vector<double> eval(slots, 0.0);
     const int64_t nchunks = single_cta ? (ns + ch - 1) / ch : 0;
@@ -383,6 +397,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
         }
         events.push_back(make_int2((int)nlev + 1, 0));  // sentinel
     }
+    phase("packing");
     if (getenv("RSB_DEBUG_ANALYSIS"))
         fprintf(stderr, "[rsb] tri kind=%d n=%lld levels=%d maxw=%lld single_cta=%d lean_n=%d far=%lld ch=%lld emax=%lld "
                 "\n",
@@ -499,6 +514,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
     }
     cudaError_t e = cudaMemsetAsync(S->ticket, 0, sizeof(unsigned long long), ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // host vectors die here
+    phase("upload");
     if (e != cudaSuccess) {
         set_error("CUDA error %s in triangular analysis upload", cudaGetErrorString(e));
         tri_free(ctx, S);

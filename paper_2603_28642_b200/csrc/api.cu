@@ -83,7 +83,18 @@ int get_tri(rsb_mat *T, int kind, TriSched **out) {
         set_error("unknown triangular solve kind %d", kind);
         return RSB_EINVAL;
     }
-    if (!T->tri[kind]) RSB_TRY(tri_analyse(T, kind, &T->tri[kind]));
+    if (!T->tri[kind]) {
+        // orders past the single-CTA limit are wide: analysed on the device
+        // (devsetup.cu), unless the host-built item-list variant is requested
+        const char *gv = getenv("RSB_TRSV_GRID");
+        const bool host = (gv && std::strcmp(gv, "lsync") == 0) || getenv("RSB_HOST_ANALYSIS");
+        if (T->nrows == T->ncols && T->ncols > kCtaTriMaxN && !host) {
+            RSB_TRY(tri_analyse_device(T, kind, &T->tri[kind]));
+        } else {
+            RSB_TRY(mat_host_copy(T));
+            RSB_TRY(tri_analyse(T, kind, &T->tri[kind]));
+        }
+    }
     *out = T->tri[kind];
     return RSB_OK;
 }
@@ -262,6 +273,27 @@ int rsb_mat_create(rsb_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *co
         set_error("col_ptr endpoints invalid or nnz %lld beyond the int32 device index range", (long long)nnz);
         return RSB_EINVAL;
     }
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    const char *du = getenv("RSB_DEVICE_UPLOAD");  // "0": host CSR build (experiments)
+    if (ncols > 0 && nnz >= kDeviceUploadMinNnz && !(du && std::strcmp(du, "0") == 0)) {
+        // large matrices: checks, int32 CSC and the CSR built on the device
+        // (devsetup.cu); host copies only when a host analysis may need them
+        auto *A = new rsb_mat();
+        A->ctx = ctx;
+        A->nrows = nrows;
+        A->ncols = ncols;
+        A->nnz = nnz;
+        int rc = mat_upload_device(A, col_ptr, row_idx, values);
+        if (rc == RSB_OK && nrows == ncols && ncols <= kCtaTriMaxN) rc = mat_host_copy(A);
+        if (rc != RSB_OK) {
+            std::string msg = rsb_last_error();
+            rsb_mat_destroy(A);
+            set_error("%s", msg.c_str());
+            return rc;
+        }
+        *out = A;
+        return RSB_OK;
+    }
     for (int64_t j = 0; j < ncols; ++j)
         if (col_ptr[j + 1] < col_ptr[j]) {
             set_error("col_ptr not non-decreasing");
@@ -272,7 +304,6 @@ int rsb_mat_create(rsb_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *co
             set_error("row index out of range");
             return RSB_EINVAL;
         }
-    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
     auto *A = new rsb_mat();
     A->ctx = ctx;
     A->nrows = nrows;

@@ -381,6 +381,13 @@ void tri_ws_free(rsb_ctx *ctx, TriWs &w);
 
 // triangular-solve analysis (analysis.cpp)
 int tri_analyse(rsb_mat *T, int kind, TriSched **out);
+// device-side setup (devsetup.cu): matrices of at least kDeviceUploadMinNnz
+// entries are checked and converted (CSR included) on the device; wide
+// schedules (order > kCtaTriMaxN) are analysed there
+constexpr int64_t kDeviceUploadMinNnz = 1 << 22;
+int mat_upload_device(rsb_mat *A, const int64_t *col_ptr, const int64_t *row_idx, const double *values);
+int mat_host_copy(rsb_mat *A);
+int tri_analyse_device(rsb_mat *T, int kind, TriSched **out);
 void tri_free(rsb_ctx *ctx, TriSched *s);
 
 // ---------------------------------------------------------------------------
