@@ -31,6 +31,7 @@ namespace {
 
 constexpr int kWideBlock = 256;
 constexpr unsigned kWideMinBackoffNs = 32, kWideMaxBackoffNs = 128;
+constexpr int kWideEvictFirst = 1;  // default of RSB_TRSV_EVICT (measured: L1 0.549 -> 0.526, U 0.796 -> 0.753 ms at n = 8e6)
 
 __device__ __forceinline__ double ld_relaxed_f64(const double *p) {
     unsigned long long v;
@@ -143,7 +144,7 @@ struct WideOcc {
 template <int MODE, int N, bool TAIL, int P>
 __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide(TriDev T, VecIn a, const double *c,
                                                                                double *x, int first_slice, int nslices,
-                                                                               unsigned max_backoff, Gate g) {
+                                                                               unsigned max_backoff, Gate g, int ev) {
     if (gated(g)) return;
     const int lane = threadIdx.x & 31;
     // slices wholly inside level 0 were solved by the prologue
@@ -193,15 +194,18 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide
             if (valid) {
                 // the right-hand side a(row) [+ c[row]] is read here (the
                 // permutation gather fused): its load overlaps the entry loads
-                row[u] = T.task_row[t];
+                row[u] = ev ? __ldcs(T.task_row + t) : T.task_row[t];
                 acc[u] = a.g ? a.p[a.g[row[u] + a.off]] : a.p[row[u] + a.off];
                 if (c) acc[u] = __dadd_rn(acc[u], c[row[u]]);
                 if (MODE & 2) d[u] = T.diag[t];
 #pragma unroll
                 for (int q = 0; q < N; ++q)
                     if (q < K) {
-                        cols[u][q] = T.ecol[base[u] + (int64_t)q * 32 + lane];
-                        vals[u][q] = T.eval[base[u] + (int64_t)q * 32 + lane];
+                        // ev: the entry stream is read evict-first, so it does not push the
+                        // solved values (polled and gathered again) out of L2
+                        const int64_t e = base[u] + (int64_t)q * 32 + lane;
+                        cols[u][q] = ev ? __ldcs(T.ecol + e) : T.ecol[e];
+                        vals[u][q] = ev ? __ldcs(T.eval + e) : T.eval[e];
                     }
 #pragma unroll
                 for (int q = 0; q < N; ++q)
@@ -297,7 +301,7 @@ __global__ void k_wide_prologue(TriDev T, VecIn a, const double *c, double *x, i
     }
 }
 
-using WideKernel = void (*)(TriDev, VecIn, const double *, double *, int, int, unsigned, Gate);
+using WideKernel = void (*)(TriDev, VecIn, const double *, double *, int, int, unsigned, Gate, int);
 
 template <int MODE, int P>
 WideKernel wide_kernel(int n, bool tail) {
@@ -361,7 +365,36 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, 
     const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
     const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ,
                                             ((int64_t)(nslices - first_slice) * 32 / p + kWideBlock - 1) / kWideBlock);
-    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, a, c, x, first_slice, nslices, max_backoff, g);
+    const char *ee = getenv("RSB_TRSV_EVICT");
+    const int ev = ee ? atoi(ee) != 0 : kWideEvictFirst;
+    const char *pe = getenv("RSB_TRSV_PERSIST");  // experiments: keep x resident in L2
+    if (pe && atoi(pe) != 0) {
+        static size_t limit_set = 0;
+        int maxw = 0, maxp = 0;
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+        const size_t want = std::min<size_t>((size_t)maxp, (size_t)T.n * sizeof(double));
+        if (limit_set < want) {
+            RSB_TRY_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+            limit_set = want;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(std::max(grid, 1));
+        cfg.blockDim = dim3(kWideBlock);
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = x;
+        attr[0].val.accessPolicyWindow.num_bytes = std::min<size_t>((size_t)maxw, (size_t)T.n * sizeof(double));
+        attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, v, a, c, x, first_slice, nslices, max_backoff, g, ev));
+        return RSB_OK;
+    }
+    k<<<std::max(grid, 1), kWideBlock, 0, ctx->stream>>>(v, a, c, x, first_slice, nslices, max_backoff, g, ev);
     return RSB_OK;
 }
 

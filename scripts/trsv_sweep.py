@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--ls-p", default="1,2,4")
     ap.add_argument("--syncfree", action="store_true")
     ap.add_argument("--occ", default="", help="comma list of RSB_LS_OCC caps to sweep too")
+    ap.add_argument("--env", action="append", default=[],
+                    help="extra sync-free settings, e.g. --env RSB_TRSV_EVICT=1 (repeatable; ';' joins several)")
     args = ap.parse_args()
     import paper_2603_28642_b200 as P
     from paper_2603_28642_b200 import _lib as L
@@ -63,9 +65,17 @@ def main():
     settings = [("ls", p, o) for p in args.ls_p.split(",") for o in ([""] + [v for v in args.occ.split(",") if v])]
     if args.syncfree:
         settings.append(("syncfree", "", ""))
+    for e in args.env:
+        settings.append(("syncfree+" + e, "", ""))
     for fam, p, occ in settings:
         key = f"{fam}" + (f"_P{p}" if p else "") + (f"_occ{occ}" if occ else "")
-        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam == "syncfree" else "levelsync"
+        for e in [v for a in args.env for v in a.split(";")]:
+            os.environ.pop(e.split("=")[0], None)
+        if fam.startswith("syncfree+"):
+            for e in fam.split("+", 1)[1].split(";"):
+                k_, v_ = e.split("=")
+                os.environ[k_] = v_
+        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam.startswith("syncfree") else "levelsync"
         os.environ["RSB_LS_P"] = p or "4"
         if occ:
             os.environ["RSB_LS_OCC"] = occ
