@@ -635,32 +635,42 @@ def run_b200(args):
 
 
 def run_rows(args):
-    """One RHS, A and L2 row-block partitioned across the ranks."""
+    """One RHS, A's rows (and L2's with them) partitioned across the ranks
+    (SURVEY.md 8(e)): distributed.py's loop on the device backend, NCCL
+    collectives on the library's stream; strong scaling."""
     import torch
     import torch.distributed as tdist
 
     import paper_2603_28642_b200 as P
     from paper_2603_28642_b200 import distributed as DI
 
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1"),
+                 ("LOCAL_RANK", "0")):
+        os.environ.setdefault(k, v)  # a single-process run without torchrun
     rank, world, local = dist_env()
     os.environ.setdefault("RSB_DEVICE", str(local))
     torch.cuda.set_device(local)
     tdist.init_process_group("nccl")
+    args.batch = 0
     A, b, _, st, name, _ = make_workload(args, 0, 1)
     S, scale, f, pre, mode, times = product_setup(args, A, st)
     norm_a = P.power_method_norm2(S, 100, args.config)
-    comm = DI.TorchComm(device=torch.device("cuda", local))
-    mk = lambda Al, pr: DI.DeviceBackend(Al, pr, local)  # noqa: E731
-    DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=args.warmup),
-                             comm, mk)
+    comm = DI.TorchComm(device=torch.device("cuda", local), reduce=os.environ.get("RSB_ROWS_REDUCE", "ordered"))
+    be = DI.DeviceBackend(local)
+    with be.stream_context():
+        part = DI.RowPartition(S, pre, comm, be)  # uploads + analyses, outside the timed region
+    DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, args.warmup)),
+                             comm, be, part)
     K = args.steps
     torch.cuda.synchronize()
     tdist.barrier()
-    t0 = time.perf_counter()
-    _, rep = DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=K),
-                                      comm, mk)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(be.stream)
+    _, rep = DI.pcgls_row_partitioned(S, b, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=K), comm, be,
+                                      part)
+    ev1.record(be.stream)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = ev0.elapsed_time(ev1) / 1e3
     t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     dt = float(t.item())
@@ -672,7 +682,10 @@ def run_rows(args):
             "data": "synthetic (seeded generators, paper_2603_28642_b200/workloads.py)",
             "config": config_dict(args, st, name, {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz},
                                   mode),
-            "parallelism": f"rows x{world}",
+            "parallelism": f"rows x{world}: A and L2 row blocks, replicated L1/U solves, "
+                           f"{comm.reduce} sums of the A^T / L2^T partials",
+            "timing": "CUDA events on the library stream around the fixed-iteration solve (includes the "
+                      "host's control flow), max over ranks",
         }), flush=True)
     tdist.destroy_process_group()
 
@@ -682,7 +695,7 @@ def main():
     os.environ["RSB_BLAS_THREADS"] = str(args.blas_threads)
     if args.impl == "reference":
         run_reference(args)
-    elif args.partition == "rows" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    elif args.partition == "rows":
         run_rows(args)
     else:
         run_b200(args)

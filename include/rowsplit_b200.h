@@ -44,6 +44,10 @@ extern "C" {
 
 #define RSB_HOST 0
 #define RSB_DEVICE 1
+/* device pointers, enqueued on the context's stream without synchronising:
+ * the caller orders its own work after it on that stream (rsb_ctx_stream);
+ * rsb_dot then writes its result to the device pointer `out` */
+#define RSB_DEVICE_ASYNC 2
 
 /* context flags: reduction order for dots and norms */
 #define RSB_DOT_EXACT 0 /* reference (OpenBLAS ddot) association: bitwise parity */
@@ -83,6 +87,9 @@ int rsb_device_count(int *count);
 int rsb_ctx_create(int device, int flags, rsb_ctx **out);
 int rsb_ctx_destroy(rsb_ctx *ctx);
 int rsb_ctx_sync(rsb_ctx *ctx);
+/* the context's CUDA stream (a cudaStream_t), for callers that enqueue their
+ * own work -- e.g. NCCL collectives -- in order with RSB_DEVICE_ASYNC calls */
+int rsb_ctx_stream(rsb_ctx *ctx, void **stream);
 /* launches of this library's kernels since the counter was last reset */
 int rsb_ctx_kernel_launches(rsb_ctx *ctx, int64_t *count, int reset);
 /* device memory of this context (bytes currently allocated) */

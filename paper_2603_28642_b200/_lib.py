@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "librowsplit_b200.so")
 
 RSB_OK, RSB_EINVAL, RSB_ESINGULAR, RSB_ECUDA, RSB_ENOMEM, RSB_ESTATE = range(6)
-RSB_HOST, RSB_DEVICE = 0, 1
+RSB_HOST, RSB_DEVICE, RSB_DEVICE_ASYNC = 0, 1, 2
 RSB_DOT_EXACT, RSB_DOT_TREE = 0, 1
 TRI_LOWER, TRI_LOWER_UNIT, TRI_UPPER, TRI_LOWER_T, TRI_LOWER_T_UNIT, TRI_UPPER_T = range(6)
 S_DENSE, S_CG, S_IDENTITY = 0, 1, 2
@@ -50,6 +50,7 @@ _SIGS = {
     "rsb_ctx_create": [ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)],
     "rsb_ctx_destroy": [vp],
     "rsb_ctx_sync": [vp],
+    "rsb_ctx_stream": [vp, ctypes.POINTER(vp)],
     "rsb_ctx_kernel_launches": [vp, i64p, ctypes.c_int],
     "rsb_ctx_mem_bytes": [vp, i64p],
     "rsb_host_alloc": [i64, ctypes.POINTER(vp)],

@@ -49,7 +49,7 @@ Staged::~Staged() {
 int stage_in(rsb_ctx *ctx, const double *p, int64_t n, int where, Staged &s) {
     s.ctx = ctx;
     s.n = (size_t)n;
-    if (where == RSB_DEVICE) {
+    if (where != RSB_HOST) {
         s.d = const_cast<double *>(p);
         return RSB_OK;
     }
@@ -62,7 +62,7 @@ int stage_in(rsb_ctx *ctx, const double *p, int64_t n, int where, Staged &s) {
 int stage_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s) {
     s.ctx = ctx;
     s.n = (size_t)n;
-    if (where == RSB_DEVICE) {
+    if (where != RSB_HOST) {
         s.d = p;
         return RSB_OK;
     }
@@ -74,6 +74,7 @@ int stage_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s) {
 int finish_out(rsb_ctx *ctx, double *p, int64_t n, int where, Staged &s) {
     if (where == RSB_HOST && n)
         RSB_TRY_CUDA(cudaMemcpyAsync(p, s.d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (where == RSB_DEVICE_ASYNC) return RSB_OK;  // stream-ordered: the caller synchronises
     RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     return RSB_OK;
 }
@@ -194,6 +195,11 @@ int rsb_ctx_destroy(rsb_ctx *ctx) {
     if (ctx->side) cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
+    return RSB_OK;
+}
+
+int rsb_ctx_stream(rsb_ctx *ctx, void **stream) {
+    *stream = (void *)ctx->stream;
     return RSB_OK;
 }
 
@@ -473,7 +479,7 @@ int rsb_chol_solve(rsb_ctx *ctx, int64_t s, const double *G, const double *b, do
     }
     Staged sg, sb, sx;
     sg.ctx = ctx;
-    if (where == RSB_DEVICE) {
+    if (where != RSB_HOST) {
         sg.d = const_cast<double *>(G);
     } else {
         RSB_TRY(dev_alloc(ctx, (void **)&sg.d, (size_t)(s * s) * sizeof(double)));
@@ -493,6 +499,8 @@ int rsb_dot(rsb_ctx *ctx, int64_t n, const double *a, const double *b, double *o
     Staged sa, sb;
     RSB_TRY(stage_in(ctx, a, n, where, sa));
     RSB_TRY(stage_in(ctx, b, n, where, sb));
+    if (where == RSB_DEVICE_ASYNC)  // the result stays on the device, at `out`
+        return launch_dot(ctx, n, VecIn{sa.d, nullptr, 0}, VecIn{sb.d, nullptr, 0}, out, 0, Gate{}, nullptr);
     RSB_TRY(launch_dot(ctx, n, VecIn{sa.d, nullptr, 0}, VecIn{sb.d, nullptr, 0}, ctx->d_scalar, 0, Gate{},
                        nullptr));
     RSB_TRY_CUDA(cudaMemcpyAsync(ctx->h_scalar, ctx->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

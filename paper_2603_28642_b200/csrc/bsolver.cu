@@ -510,7 +510,7 @@ int rsb_bsolver_start(rsb_bsolver *S, int k, const double *B, int where, const r
     // B -> staging (fr) -> interleaved b; the unused slots are zero (their
     // z.z == 0 start leaves them stopped from the outset)
     RSB_TRY_CUDA(cudaMemcpyAsync(S->fr, B, (size_t)k * m * sizeof(double),
-                                 where == RSB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+                                 where != RSB_HOST ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
     RSB_TRY(launch_bpack(ctx, S->b, S->fr, m, k));
     RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int r = 0; r < kB; ++r) {
@@ -608,7 +608,7 @@ int rsb_bsolver_finish(rsb_bsolver *S, double *X, int where, rsb_report *reps, d
     RSB_TRY(read_bstate(S));
     RSB_TRY(launch_bunpack(ctx, S->fr, S->x, S->n, S->k));
     RSB_TRY_CUDA(cudaMemcpyAsync(X, S->fr, (size_t)S->k * S->n * sizeof(double),
-                                 where == RSB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+                                 where != RSB_HOST ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
     RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int r = 0; r < S->k; ++r) {
         const CglsState &st = sts[r];

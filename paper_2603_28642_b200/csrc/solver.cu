@@ -687,7 +687,7 @@ int start_enqueue(rsb_solver *S, const double *b, int where, const rsb_cgls_cfg 
     S->cfg = *cfg;
     S->started = false;
     const int64_t m = S->m, n = S->n;
-    if (where == RSB_DEVICE) {
+    if (where != RSB_HOST) {
         RSB_TRY_CUDA(cudaMemcpyAsync(S->b, b, m * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
         RSB_TRY_CUDA(cudaMemcpyAsync(S->b, b, m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -789,7 +789,7 @@ int rsb_solver_get_x(rsb_solver *S, double *x, int where) {
     rsb_ctx *ctx = S->ctx;
     RSB_TRY_CUDA(cudaSetDevice(ctx->device));
     RSB_TRY_CUDA(cudaMemcpyAsync(x, S->x, S->n * sizeof(double),
-                                 where == RSB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+                                 where != RSB_HOST ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
     RSB_TRY_CUDA(cudaStreamSynchronize(ctx->stream));
     return RSB_OK;
 }

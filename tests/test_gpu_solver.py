@@ -158,9 +158,15 @@ def test_stagnation_visible_in_gradient_norm():
     assert rep.to_dict() == orep
 
 
-def test_row_partitioned_device_backend_single_rank_bitwise():
-    """The row-partitioned host loop on the device backend (C-ABI kernels on
-    torch CUDA tensors) with one rank equals the device pcgls bit for bit."""
+@pytest.mark.parametrize("mode", ["cg", "identity"])
+@pytest.mark.parametrize("wide", [False, True])
+def test_row_partitioned_device_backend_single_rank_bitwise(mode, wide):
+    """The row-partitioned loop on the device backend (C-ABI kernels enqueued
+    on the context stream, RSB_DEVICE_ASYNC, torch updates on the same
+    stream) with one rank equals the device pcgls bit for bit -- on narrow
+    (single-CTA) and wide (grid, device-analysed past 2^20) schedules."""
+    import torch
+
     from paper_2603_28642_b200 import distributed as D
     from paper_2603_28642_b200 import workloads as W
     from paper_2603_28642_b200.device import default_device
@@ -168,27 +174,34 @@ def test_row_partitioned_device_backend_single_rank_bitwise():
     class One:
         rank, world = 0, 1
 
-        def allreduce_(self, t):
+        def sum_(self, t):
             return t
 
-        def allreduce_scalar(self, v):
-            return v
+        def sum_scalar(self, t):
+            return float(t.item())
 
-        def allgather_cat(self, t, sizes):
-            return t
+        def allgather_padded(self, t, width):
+            buf = torch.zeros(width, dtype=t.dtype, device=t.device)
+            buf[: t.numel()] = t
+            return [buf]
 
-    A, b = W.config0(seed=11, m=600, n=400)
+    if wide:
+        A, B = W.config4(seed=4, n=1_100_000, nrhs=1)
+        b, tau = B[0], 0.0
+    else:
+        A, b = W.config0(seed=11, m=600, n=400)
+        tau = 1e-3
     S, _ = P.column_scale(A)
     na = P.power_method_norm2(S, 100, 11)
-    f = P.ilup_factorize(S, P.IlupParams(p=10, tau=1e-3, mu=1.0))
-    pre = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG)
-    cfg = P.CglsConfig(norm_A=na, delta=1e-8, max_iters=50)
+    f = P.ilup_factorize(S, P.IlupParams(p=10, tau=tau, mu=1.0))
+    pre = P.build_preconditioner(f, s_mode=P.SMode(mode))
+    cfg = P.CglsConfig(norm_A=na, delta=1e-8 if not wide else 1e-300, max_iters=50 if not wide else 4)
     x, rep = P.pcgls(S, b, pre, cfg)
-    xd, repd = D.pcgls_row_partitioned(S, b, pre, cfg, One(),
-                                       lambda Al, pr: D.DeviceBackend(Al, pr, default_device()))
+    xd, repd = D.pcgls_row_partitioned(S, b, pre, cfg, One(), D.DeviceBackend(default_device()))
     assert np.array_equal(xd, x)
     assert repd.its == rep.its and repd.ratio_pt_history == rep.ratio_pt_history
     assert repd.residual_norm_final == rep.residual_norm_final
+    assert repd.gradient_norm_final == rep.gradient_norm_final
 
 
 @pytest.mark.parametrize("mode", ["cg", "dense", None])
