@@ -449,6 +449,7 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out) {
                 le8 += len <= 8;
             }
             S->wide_n = (ml <= 4 || le4 >= n * 94 / 100) ? 4 : ((ml <= 8 || le8 >= n * 94 / 100) ? 8 : 12);
+            S->wide_static = (S->mode == 0) && le4 >= n * 3 / 4;
             if (is_dot && ml >= S->wide_n) S->wide_n = 12;  // dot-order tasks: the tail keeps the scalar chain (< 16)
             const char *wn = getenv("RSB_WIDE_N");  // experiments
             if (wn) S->wide_n = std::max(4, std::min(12, atoi(wn))) <= 4 ? 4 : (atoi(wn) <= 8 ? 8 : 12);

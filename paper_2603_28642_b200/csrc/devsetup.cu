@@ -486,6 +486,7 @@ int tri_analyse_device(rsb_mat *T, int kind, TriSched **out) {
                     ? 4
                     : ((ml <= 8 || (int64_t)h_tst.le8 >= (int64_t)n * 94 / 100) ? 8 : 12);
     if (is_dot && ml >= S->wide_n) S->wide_n = 12;
+    S->wide_static = (S->mode == 0) && (int64_t)h_tst.le4 >= (int64_t)n * 3 / 4;
     if (const char *wn = getenv("RSB_WIDE_N")) S->wide_n = std::max(4, std::min(12, atoi(wn))) <= 4 ? 4 : (atoi(wn) <= 8 ? 8 : 12);
     const char *wv = getenv("RSB_TRSV_WIDE");
     S->wide = !(is_dot && ml >= 16) && !(wv && std::strcmp(wv, "0") == 0);

@@ -231,6 +231,11 @@ struct TriSched {
     // schedule unless a dot-order task has >= 16 entries (blocked BLAS order)
     int32_t max_task = 0;
     int32_t wide_n = 12;  // entries per task the wide kernel holds in registers (4, 8 or 12)
+    // static-schedule sync-free variant (trsv_wide.cu k_trsv_static) and its
+    // register entries: chosen for sequential-order forward solves whose tasks
+    // mostly hold <= 4 entries (config 4's L1 at n = 8e6: 0.53 -> 0.41 ms)
+    bool wide_static = false;
+    int32_t static_n = 4;
     bool wide = false;
     // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
     bool lsync = false;

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "device_common.cuh"
 #include "rsb_internal.h"
@@ -275,6 +276,169 @@ __global__ void __launch_bounds__(kWideBlock, WideOcc<N * P>::value) k_trsv_wide
     }
 }
 
+// ---------------------------------------------------------------------------
+// Static-schedule variant (RSB_TRSV_GRID=static): a cooperative launch (every
+// warp resident) takes slices round-robin -- warp w owns slices w, w + W, ...
+// of the non-level-0 range -- so a warp knows its next slices and runs a
+// three-stage software pipeline across them:
+//   A(s+2W): slice offset and task row        (independent loads)
+//   B(s+W):  entries, diagonal, the right-hand side's gather index
+//   C(s):    the right-hand side value and the dependencies (one round
+//            trip), the chain, the store.
+// Progress: the lowest unfinished slice's owner is working on it (all its
+// earlier slices are finished) and its dependencies lie in lower slices.
+// ---------------------------------------------------------------------------
+template <int N>
+struct StA {
+    int64_t base;
+    int K, row;
+};
+template <int N>
+struct StB {
+    int64_t base;
+    int K, row, len;
+    int64_t gi;  // index of the right-hand side in a.p
+    double d;
+    int cols[N];
+    double vals[N];
+};
+
+template <int N>
+__device__ __forceinline__ void st_a(const TriDev &T, int s, int nslices, int lane, StA<N> &A) {
+    A.base = 0;
+    A.K = 0;
+    A.row = -1;
+    if (s < nslices) {
+        A.base = T.slice_off[s];
+        A.K = (int)((T.slice_off[s + 1] - A.base) >> 5);
+        const int t = s * 32 + lane;
+        if (t < T.n) A.row = __ldcs(T.task_row + t);
+    }
+}
+
+template <int MODE, int N, bool TAIL>
+__device__ __forceinline__ void st_b(const TriDev &T, const VecIn &a, int s, int lane, const StA<N> &A, StB<N> &B) {
+    B.base = A.base;
+    B.K = A.K;
+    B.row = A.row;
+    B.len = 0;
+    B.gi = 0;
+    B.d = 1.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        B.cols[q] = -1;
+        B.vals[q] = 0.0;
+    }
+    if (A.row < 0) return;
+    B.gi = a.g ? (int64_t)a.g[A.row + a.off] : (int64_t)A.row + a.off;
+    if (MODE & 2) B.d = T.diag[s * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+        if (q < A.K) {
+            const int64_t e = A.base + (int64_t)q * 32 + lane;
+            B.cols[q] = __ldcs(T.ecol + e);
+            B.vals[q] = __ldcs(T.eval + e);
+        }
+}
+
+// the gate, read once before the static solve: every warp of the launch must
+// agree (a warp that skipped its slices would leave others waiting forever)
+__global__ void k_gate_snap(Gate g, unsigned long long *snap) { *snap = gated(g) ? 1ull : 0ull; }
+
+template <int MODE, int N, bool TAIL>
+__global__ void __launch_bounds__(kWideBlock, 2) k_trsv_static(TriDev T, VecIn a, const double *c, double *x,
+                                                                int first_slice, int nslices, unsigned max_backoff,
+                                                                Gate g) {
+    if (*(volatile const unsigned long long *)T.ticket) return;  // the snapshot of the gate (k_gate_snap)
+    const int lane = threadIdx.x & 31;
+    const int W = gridDim.x * (kWideBlock / 32);
+    const int gw = blockIdx.x * (kWideBlock / 32) + (threadIdx.x >> 5);
+    int s = first_slice + gw;
+    StA<N> A0, A1;
+    StB<N> B;
+    st_a<N>(T, s, nslices, lane, A0);
+    st_b<MODE, N, TAIL>(T, a, s, lane, A0, B);
+    st_a<N>(T, s + W, nslices, lane, A1);
+    while (s < nslices) {
+        // next slices' stages first: their loads fly while this slice polls
+        StB<N> Bn;
+        st_b<MODE, N, TAIL>(T, a, s + W, lane, A1, Bn);
+        StA<N> A2;
+        st_a<N>(T, s + 2 * W, nslices, lane, A2);
+        // C(s)
+        int len = 0;
+        unsigned need = 0;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+            if (B.cols[q] >= 0) {
+                need |= 1u << q;
+                ++len;
+            }
+        if (TAIL && len == N && B.K > N) len = wide_tail_len(T, B.base, lane, N, B.K);
+        double acc = 0.0;
+        if (B.row >= 0) {
+            acc = a.p[B.gi];
+            if (c) acc = __dadd_rn(acc, c[B.row]);
+        }
+        bool done = B.row < 0;
+        double xv[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) xv[q] = 0.0;
+        unsigned prev = ~0u, backoff = 0;
+        for (;;) {
+            if (!__any_sync(0xffffffffu, !done)) break;
+            const bool stalled = done || need == prev;
+            if (__all_sync(0xffffffffu, stalled) && backoff) __nanosleep(backoff);
+            backoff = backoff ? min(backoff * 2, max_backoff) : kWideMinBackoffNs;
+            prev = need;
+            if (!done) {
+                unsigned long long pv[N];
+#pragma unroll
+                for (int q = 0; q < N; ++q) {
+                    pv[q] = kSentinel;
+                    poll_if((need >> q) & 1u, x + (B.cols[q] >= 0 ? B.cols[q] : 0), pv[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (((need >> q) & 1u) && pv[q] != kSentinel) {
+                        xv[q] = __longlong_as_double((long long)pv[q]);
+                        need &= ~(1u << q);
+                    }
+                if (need == 0 && (!TAIL || len <= N || wide_tail_ready(T, B.base, lane, N, len, x))) {
+                    double r = acc;
+                    if (!(MODE & 1)) {
+#pragma unroll
+                        for (int q = 0; q < N; ++q)
+                            if (q < len && xv[q] != 0.0) r = __dsub_rn(r, __dmul_rn(B.vals[q], xv[q]));
+                        if (TAIL && len > N) r = wide_tail<MODE>(T, B.base, lane, N, len, r, 0.0, x);
+                    } else if (len > 0) {
+                        double dot = 0.0;
+#pragma unroll
+                        for (int q = 0; q < N; ++q)
+                            if (q < len) dot = fma(B.vals[q], xv[q], dot);
+                        r = (TAIL && len > N) ? wide_tail<MODE>(T, B.base, lane, N, len, r, dot, x) : __dsub_rn(r, dot);
+                    }
+                    if (MODE & 2) r = __ddiv_rn(r, B.d);
+                    st_relaxed_f64(x + B.row, r);
+                    done = true;
+                }
+            }
+            __syncwarp();
+        }
+        s += W;
+        B = Bn;
+        A1 = A2;
+    }
+}
+
+using StaticKernel = void (*)(TriDev, VecIn, const double *, double *, int, int, unsigned, Gate);
+
+template <int MODE>
+StaticKernel static_kernel(int n, bool tail) {
+    if (n <= 4) return tail ? k_trsv_static<MODE, 4, true> : k_trsv_static<MODE, 4, false>;
+    return tail ? k_trsv_static<MODE, 8, true> : k_trsv_static<MODE, 8, false>;
+}
+
 // Prologue of a wide solve: every unknown is set to the sentinel the main
 // kernel polls, then the level-0 tasks, which have no dependencies, are
 // solved (x = rhs, divided by the diagonal for the non-unit kinds -- the same
@@ -365,6 +529,43 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, 
     const unsigned max_backoff = eb ? (unsigned)std::max(kWideMinBackoffNs, (unsigned)atoi(eb)) : kWideMaxBackoffNs;
     const int grid = (int)std::min<int64_t>((int64_t)sms * use_occ,
                                             ((int64_t)(nslices - first_slice) * 32 / p + kWideBlock - 1) / kWideBlock);
+    // the static-schedule variant: chosen by the analysis (T.wide_static) or
+    // forced (RSB_TRSV_GRID=static / syncfree)
+    const char *gvs = getenv("RSB_TRSV_GRID");
+    const bool want_static = gvs ? std::strcmp(gvs, "static") == 0 : T.wide_static;
+    if (want_static) {
+        const char *wn = getenv("RSB_WIDE_N");
+        const int sn = (wn ? atoi(wn) <= 4 : (T.wide_static || T.wide_n <= 4)) ? 4 : 8;
+        const bool stail = T.max_task > sn;
+        StaticKernel sk;
+        switch (T.mode & 3) {
+            case 0: sk = static_kernel<0>(sn, stail); break;
+            case 1: sk = static_kernel<1>(sn, stail); break;
+            case 2: sk = static_kernel<2>(sn, stail); break;
+            default: sk = static_kernel<3>(sn, stail); break;
+        }
+        static int socc[4][2][2] = {};
+        int &so = socc[T.mode & 3][sn == 8][stail];
+        if (so == 0) {
+            RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&so, sk, kWideBlock, 0));
+            so = std::max(so, 1);
+        }
+        const int sgrid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)sms * so, ((int64_t)(nslices - first_slice) * 32 + kWideBlock - 1) / kWideBlock));
+        k_gate_snap<<<1, 1, 0, ctx->stream>>>(g, T.ticket == v.ticket ? v.ticket : v.ticket);
+        RSB_TRY_CUDA(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sgrid);
+        cfg.blockDim = dim3(kWideBlock);
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // every warp resident: the round-robin schedule needs it
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, sk, v, a, c, x, first_slice, nslices, max_backoff, g));
+        return RSB_OK;
+    }
     const char *ee = getenv("RSB_TRSV_EVICT");
     const int ev = ee ? atoi(ee) != 0 : kWideEvictFirst;
     const char *pe = getenv("RSB_TRSV_PERSIST");  // experiments: keep x resident in L2

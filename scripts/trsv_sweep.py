@@ -71,11 +71,11 @@ def main():
         key = f"{fam}" + (f"_P{p}" if p else "") + (f"_occ{occ}" if occ else "")
         for e in [v for a in args.env for v in a.split(";")]:
             os.environ.pop(e.split("=")[0], None)
+        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam.startswith("syncfree") else "levelsync"
         if fam.startswith("syncfree+"):
             for e in fam.split("+", 1)[1].split(";"):
                 k_, v_ = e.split("=")
                 os.environ[k_] = v_
-        os.environ["RSB_TRSV_GRID"] = "syncfree" if fam.startswith("syncfree") else "levelsync"
         os.environ["RSB_LS_P"] = p or "4"
         if occ:
             os.environ["RSB_LS_OCC"] = occ

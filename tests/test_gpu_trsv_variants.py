@@ -142,7 +142,7 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
 
 
 @pytest.mark.parametrize("grid", ["levelsync", "levelsync-n4", "lsync", "syncfree", "syncfree-pairs",
-                                  "syncfree-unsorted", "syncfree-n4"])
+                                  "syncfree-unsorted", "syncfree-n4", "static", "static-n4"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -153,6 +153,12 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
         monkeypatch.setenv("RSB_TRSV_GRID", "lsync")
     if grid.startswith("levelsync"):
         monkeypatch.setenv("RSB_TRSV_GRID", "levelsync")
+    if grid.startswith("static"):
+        monkeypatch.setenv("RSB_TRSV_GRID", "static")
+    if grid.startswith("syncfree"):
+        monkeypatch.setenv("RSB_TRSV_GRID", "syncfree")
+    if grid == "static-n4":
+        monkeypatch.setenv("RSB_WIDE_N", "4")
     if grid == "levelsync-n4":  # level-synchronous with 4 register entries: long tasks take the tail
         monkeypatch.setenv("RSB_WIDE_N", "4")
     if grid == "syncfree-pairs":
