@@ -338,7 +338,7 @@ int b_capture(rsb_bsolver *S, bool trace, cudaGraph_t *graph, cudaGraphExec_t *e
     }
     RSB_TRY_CUDA(e);
     *graph = g;
-    RSB_TRY_CUDA(cudaGraphInstantiate(exec, g, 0));
+    RSB_TRY_CUDA(cudaGraphInstantiate(exec, g, cudaGraphInstantiateFlagUseNodePriority));
     return RSB_OK;
 }
 

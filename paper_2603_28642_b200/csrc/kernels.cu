@@ -18,6 +18,7 @@ namespace rsb {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int kSpmvHintDefault = 0;  // RSB_SPMV_HINT: L2 evict-first hint on k_spmv's matrix stream
 constexpr int kTriBlock = 128;
 constexpr int kCtaTri = 128;
 constexpr int kStageRegs = 16;
@@ -123,13 +124,27 @@ __global__ void k_dot_tree_final(int nparts, const double *partials, double *out
 // for the product and one for the add -- i.e. a CSR row-sequential sum.
 // ---------------------------------------------------------------------------
 template <int EPI>
-__global__ void __launch_bounds__(kBlock) k_spmv(Compressed A, VecIn x, double *y, VecIn e, Gate g) {
+__global__ void __launch_bounds__(kBlock) k_spmv(Compressed A, VecIn x, double *y, VecIn e, Gate g, int hint) {
     if (gated(g)) return;
     const int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x;
     if (i >= A.nlines) return;
     const int lo = A.ptr[i], hi = A.ptr[i + 1];
     double acc = 0.0;
-    for (int k = lo; k < hi; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], vin(x, A.idx[k])));
+    if (hint) {
+        // the matrix stream marked evict-first in L2 (a cache-policy hint; L1
+        // unchanged), so it does not push the gathered vector out of L2
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        for (int k = lo; k < hi; ++k) {
+            int c;
+            double v;
+            asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(c) : "l"(A.idx + k), "l"(pol));
+            asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(A.val + k), "l"(pol));
+            acc = __dadd_rn(acc, __dmul_rn(v, vin(x, c)));
+        }
+    } else {
+        for (int k = lo; k < hi; ++k) acc = __dadd_rn(acc, __dmul_rn(A.val[k], vin(x, A.idx[k])));
+    }
     if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, i), acc);
     if (EPI == EPI_SUB_FROM) acc = __dsub_rn(vin(e, i), acc);
     y[i] = acc;
@@ -1004,10 +1019,11 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
         }
         return post_launch(ctx);
     }
+    static const int hint = getenv("RSB_SPMV_HINT") ? atoi(getenv("RSB_SPMV_HINT")) : kSpmvHintDefault;
     switch (epi) {
-        case EPI_STORE: k_spmv<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
-        case EPI_ADD: k_spmv<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
-        default: k_spmv<EPI_SUB_FROM><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g); break;
+        case EPI_STORE: k_spmv<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g, hint); break;
+        case EPI_ADD: k_spmv<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g, hint); break;
+        default: k_spmv<EPI_SUB_FROM><<<grid, kBlock, 0, ctx->stream>>>(A, x, y, e, g, hint); break;
     }
     return post_launch(ctx);
 }

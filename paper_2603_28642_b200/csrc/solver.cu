@@ -451,7 +451,7 @@ int ensure_capacity(rsb_solver *S, int64_t max_iters, int d) {
     }
     RSB_TRY_CUDA(e);
     S->graph = graph;
-    RSB_TRY_CUDA(cudaGraphInstantiate(&S->exec, graph, 0));
+    RSB_TRY_CUDA(cudaGraphInstantiate(&S->exec, graph, cudaGraphInstantiateFlagUseNodePriority));
     S->graph_kernels = ctx->launches - before;
     ctx->launches = before;
     return RSB_OK;
@@ -894,7 +894,7 @@ int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, doubl
         }
         RSB_TRY_CUDA(e);
         S->bgraph = graph;
-        RSB_TRY_CUDA(cudaGraphInstantiate(&S->bexec, graph, 0));
+        RSB_TRY_CUDA(cudaGraphInstantiate(&S->bexec, graph, cudaGraphInstantiateFlagUseNodePriority));
         S->btrace = ctx->trace_n;
     }
     double it_total = 0.0, tri_total = 0.0;
