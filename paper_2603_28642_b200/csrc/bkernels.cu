@@ -318,6 +318,107 @@ __global__ void __launch_bounds__(kBlk) kb_dot(int64_t n, VecIn a, VecIn b, doub
     }
 }
 
+// ---- the same dot with both operands streamed through shared memory by 1-D
+// TMA bulk copies (a chunk's rows are contiguous: lo*8 .. (lo+w)*8 doubles):
+// kBDotRows rows per stage, kBDotStages stages in flight, so each SM keeps
+// ~128 KB of loads in flight instead of the ~16 KB the thread loads reach.
+// Operands are read directly (no gather); the chains, their order and the
+// finish are kb_dot's.
+constexpr int kBDotRows = 512;  // rows per stage: 32 KB per operand
+constexpr int kBDotStages = 2;
+
+__global__ void __launch_bounds__(kBlk, 1) kb_dot_staged(int64_t n, const double *a, const double *b, double *out,
+                                                          int ostride, int sqrt_out, const int *all_done,
+                                                          const int *need, int nstride, BDotChunks ch) {
+    extern __shared__ __align__(128) double sbuf[];  // [stage][a|b][kBDotRows * 8]
+    __shared__ unsigned long long bar[kBDotStages];
+    __shared__ int s_skip;
+    __shared__ double s_acc[kB][33];
+    if (threadIdx.x == 0) {
+        int sk = all_off(all_done) ? 1 : 0;
+        if (need && !sk) {
+            int any = 0;
+            for (int q = 0; q < kB; ++q) any |= *(volatile const int *)((const char *)need + (size_t)q * nstride);
+            sk = !any;
+        }
+        s_skip = sk;
+        for (int st = 0; st < kBDotStages; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const bool skip = s_skip != 0;
+    int64_t lo = 0, w = n;
+    if (ch.T > 1) {
+        int64_t rem = n;
+        for (int i = 0; i < (int)blockIdx.x; ++i) {
+            const int64_t wi = (rem + (ch.T - i) - 1) / (ch.T - i);
+            lo += wi;
+            rem -= wi;
+        }
+        w = (rem + (ch.T - (int)blockIdx.x) - 1) / (ch.T - (int)blockIdx.x);
+    }
+    const int cr = threadIdx.x & 7, cc = threadIdx.x >> 3;
+    const int64_t n32 = (w & ~(int64_t)15) & ~(int64_t)31;
+    const int64_t nst = (n32 + kBDotRows - 1) / kBDotRows;
+    double acc = 0.0;
+    if (!skip && nst > 0) {
+        auto issue = [&](int64_t c) {
+            const int st = (int)(c % kBDotStages);
+            const int64_t r0 = c * kBDotRows, r1 = min(n32, r0 + kBDotRows);
+            const unsigned bytes = (unsigned)((r1 - r0) * kB * sizeof(double));
+            double *da = sbuf + (size_t)st * 2 * kBDotRows * kB;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bar[st], 2 * bytes);
+            bulk_g2s(da, a + (lo + r0) * kB, bytes, &bar[st]);
+            bulk_g2s(da + kBDotRows * kB, b + (lo + r0) * kB, bytes, &bar[st]);
+        };
+        if (threadIdx.x == 0)
+            for (int64_t c = 0; c < min((int64_t)kBDotStages, nst); ++c) issue(c);
+        for (int64_t c = 0; c < nst; ++c) {
+            const int st = (int)(c % kBDotStages);
+            mbar_wait(&bar[st], (unsigned)((c / kBDotStages) & 1));
+            const double *da = sbuf + (size_t)st * 2 * kBDotRows * kB, *db = da + kBDotRows * kB;
+            const int rows = (int)(min(n32, (c + 1) * kBDotRows) - c * kBDotRows);
+            for (int i = cc; i < rows; i += 32) acc = fma(da[i * kB + cr], db[i * kB + cr], acc);
+            __syncthreads();  // every thread is done with this buffer
+            if (threadIdx.x == 0 && c + kBDotStages < nst) issue(c + kBDotStages);
+        }
+    }
+    s_acc[cr][cc] = acc;
+    __syncthreads();
+    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double d = 0.0;
+    if (!skip)
+        d = warp_blas_finish(
+            s_acc[r][lane], w, [&](int64_t k) { return a[(lo + k) * kB + r]; },
+            [&](int64_t k) { return b[(lo + k) * kB + r]; });
+    double *o = (double *)((char *)out + (size_t)r * ostride);
+    if (ch.T <= 1) {
+        if (!skip && lane == 0) *o = sqrt_out ? sqrt(d) : d;
+        return;
+    }
+    if (!skip && lane == 0) ch.part[blockIdx.x * kB + r] = d;
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(ch.cnt, skip ? 0x10000u + 1u : 1u);
+        last = (prev & 0xFFFFu) == (unsigned)ch.T - 1;
+        if (last) {
+            __threadfence();
+            *ch.cnt = 0;
+            if (skip || (prev >> 16)) last = false;
+        }
+    }
+    __syncthreads();
+    if (!last) return;
+    if (lane == 0) {
+        double sum = 0.0;
+        for (int i = 0; i < ch.T; ++i) sum = __dadd_rn(sum, ((volatile const double *)ch.part)[i * kB + r]);
+        *o = sqrt_out ? sqrt(sum) : sum;
+    }
+}
+
 // ---- elementwise, per-RHS scalars and gates.  The launch width is a
 // multiple of 8, so a thread always handles the same RHS r = i & 7: its
 // gate and scalar are read once.
@@ -669,6 +770,17 @@ int launch_bdot(rsb_ctx *ctx, BDotRing &ring, int64_t n, VecIn a, VecIn b, doubl
         const int slot = (int)(ring.next++ % kDotSlots);
         ch.part = ring.part + (size_t)slot * kMaxBlasThreads * kB;
         ch.cnt = ring.cnt + slot;
+    }
+    static const bool staged = !(getenv("RSB_BDOT_STAGED") && atoi(getenv("RSB_BDOT_STAGED")) == 0);
+    if (staged && !a.g && !b.g && a.off == 0 && b.off == 0) {
+        constexpr size_t smem = (size_t)kBDotStages * 2 * kBDotRows * kB * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            RSB_TRY_CUDA(cudaFuncSetAttribute(kb_dot_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        kb_dot_staged<<<T, kBlk, smem, ctx->stream>>>(n, a.p, b.p, out, ostride, sqrt_out, all_done, need, nstride, ch);
+        return bpost(ctx);
     }
     kb_dot<<<T, kBlk, 0, ctx->stream>>>(n, a, b, out, ostride, sqrt_out, all_done, need, nstride, ch);
     return bpost(ctx);
