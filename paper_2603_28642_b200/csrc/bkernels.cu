@@ -216,6 +216,11 @@ __global__ void __launch_bounds__(kBlk, 3) kb_spmv_tile(Compressed A, VecIn x, d
 }
 
 
+// (A persistent CSC variant staging each tile's indices and values by TMA
+// two tiles ahead measured slower: 3.65 vs 2.88 ms per launch at n = 8e6 --
+// two bulk copies per ~5 KB tile keep the SM's TMA unit busy longer than the
+// index round trip they hide.)
+
 // CSR products (A p, L2 t): an octet of lanes per row straight from global
 // memory.  Rows here are short (6-7 entries); on config 4 at n = 8e6 this
 // measured 2.1 ms for A p against 4.2 ms for the tiled kernel.
