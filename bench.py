@@ -342,6 +342,13 @@ def run_reference(args):
     _, rep = O.pcgls(S, b, op, norm_a, delta=1e-300, max_iters=k)
     dt = time.perf_counter() - t0
     value = k / dt
+    # the reference's time to tolerance on the host: power method + pcgls to delta
+    t0 = time.perf_counter()
+    _, rtol = O.pcgls(S, b, op, norm_a, delta=st["delta"], max_iters=st["max_iters"])
+    t_solve = time.perf_counter() - t0
+    tol = {"seconds": times["power_method_s"] + t_solve, "power_method_s": times["power_method_s"],
+           "solve_s": t_solve, "its": rtol["its"], "converged": rtol["converged"], "delta": st["delta"],
+           "includes": "power method (100 its) + pcgls to delta on the host cores; ILUP in `setup`"}
     nnz = {"A": S.nnz, "L1": f.L1.nnz, "L2": f.L2.nnz, "U": f.U.nnz}
     sample = (f"{k} fixed iterations (delta=1e-300) of the oracle port of pcgls on this config "
               f"after {args.warmup} warm-up iterations")
@@ -354,6 +361,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": threads, "kind": "port",
                          "sample": sample, "host_cpu": model, "host_cores": cores},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "time_to_tol": tol,
         "setup": {**times, "generate_s": t_gen, "factor_digest": factor_digest(S.values, f)},
         "native_libs": loaded_native_libs(),
     }

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "bsolver.cuh"
 #include "device_common.cuh"
@@ -696,6 +697,184 @@ __global__ void __launch_bounds__(kBlk, 2) kb_trsv(TriDev T, VecIn a, const doub
     }
 }
 
+// Static-schedule batched solve for short-task forward solves (the single-RHS
+// k_trsv_static's scheme): a cooperative launch, warp w owns slices w, w + W,
+// ...; the next slice's row, offsets, entries and right-hand-side index are
+// loaded while this slice waits, and all 8 right-hand sides' dependencies of
+// a ready task are read at once (4 register entries; longer tasks take the
+// tail per half).
+template <int MODE, bool TAIL>
+__global__ void __launch_bounds__(kBlk, 2) kb_trsv_static(TriDev T, VecIn a, const double *c, double *x, int *flag,
+                                                          const unsigned *epoch, int first_slice, int nslices,
+                                                          const int *all_done) {
+    constexpr int N = 4;
+    if (all_off(all_done)) return;  // set only between iterations: uniform over the launch
+    const int E = (int)*(volatile const unsigned *)epoch;
+    const int lane = threadIdx.x & 31;
+    const int W = gridDim.x * (kBlk / 32);
+    const int gw = blockIdx.x * (kBlk / 32) + (threadIdx.x >> 5);
+    struct Pre {
+        int64_t base;
+        int K, row;
+    };
+    struct Task {
+        int64_t base, ai;
+        int K, row;
+        double d;
+        int cols[N];
+        double vals[N];
+    };
+    auto stage_a = [&](int s, Pre &P) {
+        P.base = 0;
+        P.K = 0;
+        P.row = -1;
+        if (s < nslices) {
+            P.base = T.slice_off[s] + lane;
+            P.K = (int)((T.slice_off[s + 1] - T.slice_off[s]) >> 5);
+            const int t = s * 32 + lane;
+            if (t < T.n) P.row = __ldcs(T.task_row + t);
+        }
+    };
+    auto stage_b = [&](int s, const Pre &P, Task &k) {
+        k.base = P.base;
+        k.K = P.K;
+        k.row = P.row;
+        k.ai = 0;
+        k.d = 1.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            k.cols[q] = -1;
+            k.vals[q] = 0.0;
+        }
+        if (P.row < 0) return;
+        k.ai = a.g ? (int64_t)a.g[P.row + a.off] : (int64_t)P.row + a.off;
+        if (MODE & 2) k.d = T.diag[s * 32 + lane];
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+            if (q < P.K) {
+                k.cols[q] = __ldcs(T.ecol + P.base + (int64_t)q * 32);
+                k.vals[q] = __ldcs(T.eval + P.base + (int64_t)q * 32);
+            }
+    };
+    int s = first_slice + gw;
+    Pre A1;
+    Task cur;
+    {
+        Pre A0;
+        stage_a(s, A0);
+        stage_b(s, A0, cur);
+    }
+    stage_a(s + W, A1);
+    while (s < nslices) {
+        Task nxt;
+        stage_b(s + W, A1, nxt);
+        Pre A2;
+        stage_a(s + 2 * W, A2);
+        int len = 0;
+        unsigned need = 0;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+            if (cur.cols[q] >= 0) {
+                need |= 1u << q;
+                ++len;
+            }
+        if (TAIL && len == N && cur.K > N) len = bt_tail_len(T, cur.base, N, cur.K);
+        bool done = cur.row < 0;
+        unsigned prev = ~0u, backoff = 0;
+        for (;;) {
+            if (!__any_sync(0xffffffffu, !done)) break;
+            const bool stalled = done || need == prev;
+            if (__all_sync(0xffffffffu, stalled) && backoff) __nanosleep(backoff);
+            backoff = backoff ? min(backoff * 2, kBtMaxBackoff) : kBtMinBackoff;
+            prev = need;
+            if (!done) {
+                int f[N];
+#pragma unroll
+                for (int q = 0; q < N; ++q) f[q] = ((need >> q) & 1u) ? ld_flag(flag + cur.cols[q]) : E;
+#pragma unroll
+                for (int q = 0; q < N; ++q)
+                    if (f[q] == E) need &= ~(1u << q);
+                if (need == 0 && (!TAIL || len <= N || bt_tail_ready(T, cur.base, N, len, flag, E))) {
+                    __threadfence();  // acquire: the flags were seen, now the values
+                    double xv[N][8], acc[8], cv[8];
+#pragma unroll
+                    for (int e = 0; e < N; ++e) {
+                        if (cur.cols[e] >= 0) {
+                            double h0[4], h1[4];
+                            ld4(x + (int64_t)cur.cols[e] * kB, h0);
+                            ld4(x + (int64_t)cur.cols[e] * kB + 4, h1);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                xv[e][q] = h0[q];
+                                xv[e][4 + q] = h1[q];
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) xv[e][q] = 0.0;
+                        }
+                    }
+                    {
+                        double h0[4], h1[4];
+                        ld4(a.p + cur.ai * kB, h0);
+                        ld4(a.p + cur.ai * kB + 4, h1);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            acc[q] = h0[q];
+                            acc[4 + q] = h1[q];
+                        }
+                    }
+                    if (c) {
+                        double h0[4], h1[4];
+                        ld4(c + (int64_t)cur.row * kB, h0);
+                        ld4(c + (int64_t)cur.row * kB + 4, h1);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            cv[q] = h0[q];
+                            cv[4 + q] = h1[q];
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[q] = __dadd_rn(acc[q], cv[q]);
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        double ah[4], dot[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ah[q] = acc[4 * h + q];
+#pragma unroll
+                        for (int e = 0; e < N; ++e) {
+                            if (e >= len) break;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                if (!(MODE & 1)) {
+                                    if (xv[e][4 * h + q] != 0.0)
+                                        ah[q] = __dsub_rn(ah[q], __dmul_rn(cur.vals[e], xv[e][4 * h + q]));
+                                } else {
+                                    dot[q] = fma(cur.vals[e], xv[e][4 * h + q], dot[q]);
+                                }
+                            }
+                        }
+                        if (TAIL && len > N) bt_tail<MODE>(T, cur.base, N, len, h, x, ah, dot);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            if ((MODE & 1) && len > 0) ah[q] = __dsub_rn(ah[q], dot[q]);
+                            if (MODE & 2) ah[q] = __ddiv_rn(ah[q], cur.d);
+                        }
+                        double2 *o = reinterpret_cast<double2 *>(x + (int64_t)cur.row * kB + 4 * h);
+                        __stcg(o, make_double2(ah[0], ah[1]));
+                        __stcg(o + 1, make_double2(ah[2], ah[3]));
+                    }
+                    st_flag_release(flag + cur.row, E);
+                    done = true;
+                }
+            }
+            __syncwarp();
+        }
+        s += W;
+        cur = nxt;
+        A1 = A2;
+    }
+}
+
 // level 0 of a batched solve: no dependencies.  An octet of lanes per task
 // (lane r: RHS r); after the octet's 8 stores, its first lane publishes the
 // row's flag (the octet barrier orders the stores before the release).
@@ -861,7 +1040,40 @@ int launch_btrsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doub
     }
     const int nslices = (T.n + 31) / 32;
     const int first_slice = lvl1 / 32;
-    if (first_slice < nslices) {
+    const char *gvs = getenv("RSB_TRSV_GRID");
+    // the static-schedule variant is opt-in here (RSB_TRSV_GRID=static): with 8
+    // right-hand sides per task it measured slower than the ticket kernel
+    // (L1 at n = 8e6: 1.76 vs 1.53 ms; 128 registers with spills)
+    const bool want_static = gvs && std::strcmp(gvs, "static") == 0;
+    if (first_slice < nslices && want_static) {
+        const bool tail = T.max_task > 4;
+        auto k = (T.mode & 3) == 0 ? (tail ? kb_trsv_static<0, true> : kb_trsv_static<0, false>)
+                 : (T.mode & 3) == 1 ? (tail ? kb_trsv_static<1, true> : kb_trsv_static<1, false>)
+                 : (T.mode & 3) == 2 ? (tail ? kb_trsv_static<2, true> : kb_trsv_static<2, false>)
+                                     : (tail ? kb_trsv_static<3, true> : kb_trsv_static<3, false>);
+        static int socc[4][2] = {};
+        int &so = socc[T.mode & 3][tail];
+        if (so == 0) {
+            RSB_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&so, k, kBlk, 0));
+            so = std::max(so, 1);
+        }
+        int sms = 0;
+        RSB_TRY_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int grid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)sms * so, ((int64_t)(nslices - first_slice) * 32 + kBlk - 1) / kBlk));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kBlk);
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;  // round-robin slices: every warp must be resident
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, v, a, c, x, ws.flag, (const unsigned *)ws.epoch, first_slice, nslices,
+                                        all_done));
+        RSB_TRY(bpost(ctx));
+    } else if (first_slice < nslices) {
         const int wn = T.wide_n <= 4 ? 4 : 8;
         const bool tail = T.max_task > wn;
         BtKernel k;

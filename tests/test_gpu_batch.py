@@ -116,3 +116,18 @@ def test_batch_rejects_narrow_and_dense():
         X, reps = P.pcgls_batch(S, np.stack([b, b]), pre, P.CglsConfig(norm_A=1.0, delta=1e-8, max_iters=20))
         x1, r1 = P.pcgls(S, b, pre, P.CglsConfig(norm_A=1.0, delta=1e-8, max_iters=20))
         assert np.array_equal(X[1], x1) and _rep(reps[1]) == _rep(r1)
+
+
+def test_batch_static_schedule_option(cfg4, monkeypatch):
+    """RSB_TRSV_GRID=static: the batched static-schedule solve (opt-in) gives
+    the same bits."""
+    S, B, na, f = cfg4
+    pre = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG)
+    cfg = P.CglsConfig(norm_A=na, delta=1e-300, max_iters=5)
+    X0, r0 = P.pcgls_batch(S, B[:8], pre, cfg)
+    monkeypatch.setenv("RSB_TRSV_GRID", "static")
+    D.clear_caches()
+    A2 = P.CscMatrix(S.nrows, S.ncols, S.col_ptr, S.row_idx, S.values)
+    pre2 = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG)
+    X1, r1 = P.pcgls_batch(A2, B[:8], pre2, cfg)
+    assert np.array_equal(X0, X1) and [_rep(r) for r in r0] == [_rep(r) for r in r1]
