@@ -303,6 +303,7 @@ int rsb_mat_create(rsb_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *co
         A->nnz = nnz;
         int rc = mat_upload_device(A, col_ptr, row_idx, values);
         if (rc == RSB_OK && nrows == ncols && ncols <= kCtaTriMaxN) rc = mat_host_copy(A);
+        if (rc == RSB_OK) rc = mat_build_bands(A);
         if (rc != RSB_OK) {
             std::string msg = rsb_last_error();
             rsb_mat_destroy(A);
@@ -386,6 +387,7 @@ int rsb_mat_destroy(rsb_mat *A) {
     dev_free(ctx, A->r_idx, A->nnz * sizeof(int32_t));
     dev_free(ctx, A->r_val, A->nnz * sizeof(double));
     for (auto &t : A->tri) tri_free(ctx, t);
+    for (auto &b : A->band_bufs) dev_free(ctx, b.first, b.second);
     delete A;
     return RSB_OK;
 }

@@ -1028,9 +1028,68 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
     return post_launch(ctx);
 }
 
+// ---- row-banded transposed product (Banded, devsetup.cu mat_build_bands).
+// Phase 1: every product val * y[row], one thread per entry over the
+// band-major arrays, so the blocks run band by band and each band's slice of
+// y stays in L2 (the plain kernel's gathers of a 128 MB y miss L2: 7.3 GB of
+// DRAM reads for 1.4 GB of algorithmic bytes at config 4).  Phase 2: column
+// j's products are its band segments in band order -- its original entry
+// order -- summed p0 + pairwise(p1..) exactly as k_spmv_t_tile does.
+__global__ void __launch_bounds__(kBlock) k_band_prod(Banded B, int64_t nnz, VecIn y, Gate g) {
+    if (gated(g)) return;
+    const int64_t e = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    if (e < nnz) B.prod[e] = __dmul_rn(__ldcs(B.val + e), vin(y, __ldcs(B.idx + e)));
+}
+
+struct BandTerm {
+    const double *prod;
+    int nb;
+    int lo[kMaxBands], cnt[kMaxBands];
+    __device__ double operator()(int64_t k) const {
+        for (int b = 0; b < nb; ++b) {
+            if (k < cnt[b]) return prod[lo[b] + k];
+            k -= cnt[b];
+        }
+        return 0.0;
+    }
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) k_band_sum(Banded B, int32_t ncols, double *z, VecIn e, Gate g) {
+    if (gated(g)) return;
+    const int64_t j = blockIdx.x * (int64_t)kBlock + threadIdx.x;
+    if (j >= ncols) return;
+    BandTerm t;
+    t.prod = B.prod;
+    t.nb = B.nbands;
+    int n = 0;
+    for (int b = 0; b < B.nbands; ++b) {
+        t.lo[b] = B.bptr[b][j];
+        t.cnt[b] = B.bptr[b][j + 1] - t.lo[b];
+        n += t.cnt[b];
+    }
+    double acc = 0.0;
+    if (n > 0) acc = __dadd_rn(t(0), n - 1 <= 128 ? pw_leaf(t, 1, n - 1) : Pairwise<25, BandTerm>::sum(t, 1, n - 1));
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, j), acc);
+    z[j] = acc;
+}
+
 int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
     if (At.nlines == 0) return RSB_OK;
     const int grid = grid_for(At.nlines, kBlock);
+    // the banded path uses the matrix's product scratch: only on the stream of
+    // the context that owns it (concurrent solvers on other streams take the
+    // plain kernel)
+    if (At.bands && At.bands->owner == (const void *)ctx) {
+        const Banded B = *At.bands;
+        k_band_prod<<<(unsigned)((At.nnz + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(B, At.nnz, y, g);
+        RSB_TRY(post_launch(ctx));
+        if (epi == EPI_ADD)
+            k_band_sum<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
+        else
+            k_band_sum<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
+        return post_launch(ctx);
+    }
     if (spmv_tiled()) {
         static const bool occ6 = getenv("RSB_SPMV_T_OCC") && atoi(getenv("RSB_SPMV_T_OCC")) == 6;  // experiments
         if (occ6) {

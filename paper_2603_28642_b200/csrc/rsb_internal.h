@@ -103,6 +103,22 @@ struct alignas(16) StageMeta {
 
 // Compressed sparse rows (or columns, for the transposed product): entries of
 // line i are idx/val[ptr[i] .. ptr[i+1]) in the order the reference adds them.
+// Row-banded copy of a CSC matrix (devsetup.cu): the entries of every column
+// split by row band -- band b holds rows [b*rows_per_band, (b+1)*...) --
+// band-major, so the transposed product can form its products band by band
+// with each band's slice of the gathered vector resident in L2, then sum
+// each column's products in the original order (kernels.cu).
+constexpr int kMaxBands = 8;
+struct Banded {
+    int nbands;
+    int64_t rows_per_band;
+    const int32_t *bptr[kMaxBands];  // ncols + 1 each, offsets into the band-major arrays
+    const int32_t *idx;              // rows, band-major
+    const double *val;
+    double *prod;                    // products scratch (nnz), owned by the matrix's context
+    const void *owner;               // rsb_ctx whose stream may use `prod`
+};
+
 struct Compressed {
     int32_t nlines;  // rows for CSR, columns for CSC
     int32_t nother;
@@ -111,6 +127,7 @@ struct Compressed {
     const int32_t *idx;
     const double *val;
     int32_t max_len;  // longest line
+    const Banded *bands = nullptr;  // CSC only, large matrices (see Banded)
 };
 
 // A vector operand, optionally read through a gather: v(i) = p[g[i + off]]
@@ -325,8 +342,12 @@ struct rsb_mat {
         return rsb::Compressed{(int32_t)nrows, (int32_t)ncols, nnz, r_ptr, r_idx, r_val, max_row_len};
     }
     rsb::Compressed csc() const {
-        return rsb::Compressed{(int32_t)ncols, (int32_t)nrows, nnz, c_ptr, c_idx, c_val, max_col_len};
+        return rsb::Compressed{(int32_t)ncols, (int32_t)nrows, nnz, c_ptr, c_idx, c_val, max_col_len,
+                               bands.nbands ? &bands : nullptr};
     }
+    // row bands of the CSC (large matrices: the gathered vector exceeds L2)
+    rsb::Banded bands{};
+    std::vector<std::pair<void *, size_t>> band_bufs;
 };
 
 namespace rsb {
@@ -392,6 +413,10 @@ int tri_analyse(rsb_mat *T, int kind, TriSched **out);
 constexpr int64_t kDeviceUploadMinNnz = 1 << 22;
 int mat_upload_device(rsb_mat *A, const int64_t *col_ptr, const int64_t *row_idx, const double *values);
 int mat_host_copy(rsb_mat *A);
+// row bands of A's CSC when its gathered vector (8 * nrows bytes) exceeds
+// kBandBytes and RSB_BANDS=1 (opt-in: measured slower); frees with the matrix
+constexpr int64_t kBandBytes = 40ll << 20;
+int mat_build_bands(rsb_mat *A);
 int tri_analyse_device(rsb_mat *T, int kind, TriSched **out);
 void tri_free(rsb_ctx *ctx, TriSched *s);
 

@@ -110,3 +110,32 @@ def test_device_analysis_zero_diagonal(mats):
     Z = P.CscMatrix(Ln.nrows, Ln.ncols, Ln.col_ptr, Ln.row_idx, v)
     with pytest.raises(np.linalg.LinAlgError, match="column 555"):
         P.sparse_lower_solve(Z, b)
+
+
+def test_banded_transposed_product_bitwise(monkeypatch):
+    """A^T y with the gathered vector past 40 MB and RSB_BANDS=1 runs the row-banded product
+    (products band by band, then each column's pairwise sum in its original
+    order): equal to the oracle, including columns longer than 128 entries
+    (numpy's pairwise split) that straddle bands, and in the plain-kernel
+    order on another stream (the scratch belongs to the matrix's own)."""
+    monkeypatch.setenv("RSB_BANDS", "1")  # opt-in (measured slower at config 4)
+    rng = np.random.default_rng(9)
+    m, n, k = 6_000_000, 900_000, 5
+    rows = rng.integers(0, m, size=n * k)
+    cols = np.repeat(np.arange(n, dtype=np.int64), k)
+    # a few long columns spanning every band
+    long_cols = np.repeat(np.arange(10, dtype=np.int64), 300)
+    rows = np.concatenate([rows, rng.integers(0, m, size=len(long_cols))])
+    cols = np.concatenate([cols, long_cols])
+    A = P.CscMatrix.from_coo(m, n, rows, cols, rng.standard_normal(len(rows)))
+    y = rng.standard_normal(m)
+    want = O.matvec_transpose(A, y)
+    assert np.array_equal(P.matvec_transpose(A, y), want)
+    from paper_2603_28642_b200.device import Context
+
+    other = Context()
+    dA = DeviceMatrix(A, get_context())
+    z = np.empty(n)
+    L.check(L.lib().rsb_matvec_transpose(dA.h, L.ptr(y), L.ptr(z), L.RSB_HOST))
+    assert np.array_equal(z, want)
+    assert other.h is not None
