@@ -79,6 +79,7 @@ typedef struct rsb_pre rsb_pre;
 typedef struct rsb_solver rsb_solver;
 typedef struct rsb_ilup rsb_ilup;
 typedef struct rsb_bsolver rsb_bsolver;
+typedef struct rsb_dbuild rsb_dbuild;
 
 /* ---- library / context ------------------------------------------------ */
 const char *rsb_last_error(void);
@@ -245,6 +246,25 @@ int rsb_pcgls_batch8(rsb_bsolver *S, int k, const double *B, int where, const rs
 /* measurement, as rsb_solver_bench, for the whole batch */
 int rsb_bsolver_bench(rsb_bsolver *S, int64_t kit, int flush, double *iter_ms, double *tri_ms,
                       int64_t *tri_launches, int64_t *kernels_per_iter, int *all_done);
+
+/* ---- dense-coupling preconditioner build on the device -- */
+/* build_y_explicit (pc.py:55-82): Y = L2 L1^{-1}, one sparse-RHS L1^T solve
+ * per row of L2 in the reference's DFS reach order (sc.py:328-397), zeros
+ * dropped; bit-identical.  what >= 1 also forms S = I + Y Y^T (pc.py:85-92;
+ * fixed-order FP64 product, within rounding of numpy's `yd @ yd.T`) and its
+ * Cholesky factor (sc.py:585-604; bit-identical given S); what = 2 keeps S.
+ * L1, L2: device matrices of one context (rsb_mat_create). */
+int rsb_dense_build(rsb_mat *L1, rsb_mat *L2, int what, rsb_dbuild **out);
+/* sizes and the seconds of the three phases (Y, S, factor) */
+int rsb_dense_build_sizes(const rsb_dbuild *B, int64_t *s, int64_t *n, int64_t *nnz_y, double *seconds3);
+/* Y as host CSC (y_ptr n + 1, y_idx / y_val nnz_y), S and the factor as s x s
+ * column-major host arrays; any output may be NULL */
+int rsb_dense_build_copy(const rsb_dbuild *B, int64_t *y_ptr, int64_t *y_idx, double *y_val, double *S,
+                         double *S_factor);
+int rsb_dense_build_destroy(rsb_dbuild *B);
+/* dense_cholesky_factorize (sc.py:585-604) on the device, in place on an
+ * s x s column-major array (host or device per `where`), bit-identical */
+int rsb_cholesky_factorize_device(rsb_ctx *ctx, int64_t s, double *g, int where);
 
 /* ---- host setup (stays on the CPU; timed separately) -------------------- */
 /* ilup_factorize (il.py:211-368), bit-identical factors.  Inputs: scaled A

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -63,6 +64,51 @@ def build_y_explicit(factors) -> CscMatrix:
     L.check(L.lib().rsb_build_y_explicit(s, n, *args, ctypes.byref(nnz), L.ptr(yp), L.ptr(yi), L.ptr(yv)))
     k = nnz.value
     return CscMatrix(s, n, yp, yi[:k], yv[:k])
+
+
+def _setup_where(setup) -> str:
+    where = setup if setup is not None else os.environ.get("RSB_SETUP", "host")
+    if where not in ("host", "device"):
+        raise ValueError("setup must be 'host' or 'device'")
+    return where
+
+
+def dense_build_device(factors, what: int = 1):
+    """Y = L2 L1^{-1}, S = I + Y Y^T and its Cholesky factor, formed on the
+    device (csrc/dbuild.cu; pc.py:55-103, sc.py:585-604).
+
+    what = 0: Y only; 1: Y and the S factor; 2: also S.  Returns (Y,
+    S or None, S_factor or None, seconds of the three phases).  Y and the
+    factor-given-S are bit-identical to the reference; S is a fixed-order
+    FP64 product within rounding of numpy's ``yd @ yd.T``.
+    """
+    from .device import device_matrix, get_context
+
+    factors = IlupFactors.of(factors)
+    ctx = get_context()
+    d1, d2 = device_matrix(factors.L1, ctx), device_matrix(factors.L2, ctx)
+    h = ctypes.c_void_p()
+    L.check(L.lib().rsb_dense_build(d1.h, d2.h, int(what), ctypes.byref(h)))
+    try:
+        s, n, nnz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        sec = np.zeros(3)
+        L.check(L.lib().rsb_dense_build_sizes(h, ctypes.byref(s), ctypes.byref(n), ctypes.byref(nnz),
+                                              sec.ctypes.data_as(L.f64p)))
+        s, n, k = s.value, n.value, nnz.value
+        yp = np.empty(n + 1, dtype=np.int64)
+        yi = np.empty(max(1, k), dtype=np.int64)
+        yv = np.empty(max(1, k))
+        S = np.empty((s, s), order="F") if what == 2 else None
+        F = np.empty((s, s), order="F") if what >= 1 else None
+        L.check(L.lib().rsb_dense_build_copy(
+            h, L.ptr(yp), L.ptr(yi), L.ptr(yv),
+            L.ptr(S.ravel(order="K")) if S is not None and s else None,
+            L.ptr(F.ravel(order="K")) if F is not None and s else None))
+    finally:
+        L.lib().rsb_dense_build_destroy(h)
+    Y = CscMatrix(s, n, yp, yi[:k], yv[:k])
+    return (Y, DenseMatrix(S) if S is not None else None, DenseMatrix(F) if F is not None else None,
+            tuple(float(v) for v in sec))
 
 
 def _gram_plus_identity(Y) -> DenseMatrix:
@@ -149,12 +195,20 @@ def build_preconditioner(
     y_mode: YMode | None = None,
     cg_iters: int = 2,
     dense_cap: int = 20000,
+    *,
+    setup: str | None = None,
 ) -> RowSplitPreconditioner:
     """Assemble the applied preconditioner (pc.py:323-362).
 
     y_mode defaults to explicit for the dense S factorization and implicit
-    otherwise; ValueError for a dense request above dense_cap.
+    otherwise; ValueError for a dense request above dense_cap.  setup
+    ('host', default, or 'device'; env RSB_SETUP) says where the explicit Y,
+    S = I + Y Y^T and its Cholesky factor are formed: the host build is
+    bit-identical to the reference throughout; the device build
+    (dense_build_device) gives the same Y bits and the same factor bits for
+    a given S, with S itself within rounding of the reference's BLAS product.
     """
+    where = _setup_where(setup)
     factors = IlupFactors.of(factors)
     s_mode = _smode(s_mode)
     y_mode = _ymode(y_mode)
@@ -167,10 +221,13 @@ def build_preconditioner(
     s = factors.L2.nrows
     if s_mode is SMode.DENSE_FACTOR and s > dense_cap:
         raise ValueError(f"coupling block of size {s} exceeds the dense cap {dense_cap}")
-    Y = build_y_explicit(factors) if y_mode is YMode.EXPLICIT else None
-    S_factor = None
-    if s_mode is SMode.DENSE_FACTOR:
-        S_factor = dense_cholesky_factorize(_gram_plus_identity(Y))
+    Y = S_factor = None
+    if y_mode is YMode.EXPLICIT and where == "device":
+        Y, _, S_factor, _ = dense_build_device(factors, 1 if s_mode is SMode.DENSE_FACTOR else 0)
+    elif y_mode is YMode.EXPLICIT:
+        Y = build_y_explicit(factors)
+        if s_mode is SMode.DENSE_FACTOR:
+            S_factor = dense_cholesky_factorize(_gram_plus_identity(Y))
     return RowSplitPreconditioner(
         factors=factors, y_mode=y_mode, s_mode=s_mode, cg_iters=cg_iters, Y=Y,
         S_factor=S_factor, psize=_psize(factors, Y, S_factor), dense_cap=dense_cap,

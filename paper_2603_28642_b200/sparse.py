@@ -11,6 +11,8 @@ bit-identical to the reference's.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib as L
@@ -117,14 +119,24 @@ def column_scale(A):
     return out, ColumnScaling(norms)
 
 
-def dense_cholesky_factorize(S) -> DenseMatrix:
-    """Lower Cholesky factor (sc.py:585-604), host native, bit-identical."""
+def dense_cholesky_factorize(S, *, setup: str | None = None) -> DenseMatrix:
+    """Lower Cholesky factor (sc.py:585-604), bit-identical.  setup='host'
+    (default; env RSB_SETUP) runs the native host sweep, 'device' the
+    blocked right-looking kernels of csrc/dbuild.cu (same per-element
+    subtraction order)."""
     a = getattr(S, "a", S)
     a = np.asarray(a, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError("Cholesky needs a square matrix")
     g = np.array(a, order="F", copy=True)
-    L.check(L.lib().rsb_cholesky_factorize(g.shape[0], L.ptr(g.ravel(order="K"))))
+    where = setup if setup is not None else os.environ.get("RSB_SETUP", "host")
+    if where == "device":
+        L.check(L.lib().rsb_cholesky_factorize_device(get_context().h, g.shape[0], L.ptr(g.ravel(order="K")),
+                                                      L.RSB_HOST))
+    elif where == "host":
+        L.check(L.lib().rsb_cholesky_factorize(g.shape[0], L.ptr(g.ravel(order="K"))))
+    else:
+        raise ValueError("setup must be 'host' or 'device'")
     return DenseMatrix(g)
 
 
