@@ -139,6 +139,7 @@ int rsb_trsv_levels(rsb_mat *T, int kind, int64_t *nlevels, int64_t *max_width);
 #define RSB_TRSV_LEVELS 3
 #define RSB_TRSV_LSYNC 4 /* persistent level-synchronous grid solve, items taken in level order (option) */
 #define RSB_TRSV_LEVELSYNC 5 /* cooperative grid solve walking the levels with grid barriers (wide DAGs; default) */
+#define RSB_TRSV_NATURAL 6 /* sync-free grid solve in index order, entries read from the matrix's own arrays (wide DAGs with far dependencies; default there) */
 int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n);
 /* power_method_norm2 (sc.py:428-454); v0 = default_rng(seed).standard_normal(n),
  * drawn by the caller (host RNG stays on the host). */

@@ -97,6 +97,7 @@ int get_tri(rsb_mat *T, int kind, TriSched **out) {
             RSB_TRY(mat_host_copy(T));
             RSB_TRY(tri_analyse(T, kind, &T->tri[kind]));
         }
+        RSB_TRY(tri_setup_nat(T, kind, T->tri[kind]));
     }
     *out = T->tri[kind];
     return RSB_OK;
@@ -466,7 +467,8 @@ int rsb_trsv_variant(rsb_mat *T, int kind, int *variant, int *lean_n) {
     TriSched *S = nullptr;
     RSB_TRY_CUDA(cudaSetDevice(T->ctx->device));
     RSB_TRY(get_tri(T, kind, &S));
-    *variant = S->lean_n ? RSB_TRSV_LEAN
+    *variant = S->use_nat ? RSB_TRSV_NATURAL
+               : S->lean_n ? RSB_TRSV_LEAN
                          : (S->single_cta ? RSB_TRSV_STAGED
                                           : (S->level_launch ? RSB_TRSV_LEVELS
                                                              : (S->lsync ? RSB_TRSV_LSYNC

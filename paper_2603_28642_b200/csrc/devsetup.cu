@@ -118,22 +118,6 @@ int bits_for(int64_t v) {
 }
 
 // ---- triangular analysis on the device ---------------------------------
-// Task t's entries in the reference's accumulation order: idx/val[base +
-// step * k], k < len (analysis.cpp: column t of the CSC for the transposed
-// solves, row t of the CSR -- columns ascending / descending -- otherwise;
-// the diagonal excluded for the non-unit kinds).
-struct TaskSrc {
-    const int32_t *ptr, *idx;
-    const double *val;
-    int first_off, last_off, step;  // base = ptr[t] + first_off (step +1) or ptr[t+1] - 1 (step -1)
-    int diag_at;                    // 0: ptr[t] (first), 1: ptr[t+1] - 1 (last), -1: unit
-    __device__ void task(int t, int64_t &base, int &len) const {
-        const int lo = ptr[t], hi = ptr[t + 1];
-        len = (hi - lo) - first_off - last_off;
-        base = step > 0 ? (int64_t)lo + first_off : (int64_t)hi - 1 - last_off;
-    }
-};
-
 // non-unit: every column (row) holds its diagonal, nonzero; the stored
 // off-diagonal entries are strictly on the triangular side.  bad_diag /
 // bad_tri get the smallest and largest failing line (the caller reports the
@@ -427,18 +411,14 @@ int mat_host_copy(rsb_mat *A) {
     return RSB_OK;
 }
 
-// Level analysis of a wide schedule on the device (n > kCtaTriMaxN: never
-// single-CTA).  Produces analysis.cpp's grid schedule.
-int tri_analyse_device(rsb_mat *T, int kind, TriSched **out) {
-    rsb_ctx *ctx = T->ctx;
-    cudaStream_t st = ctx->stream;
-    const int n = (int)T->ncols;
+// where the tasks of a solve kind live in the matrix's arrays
+TaskSrc tri_task_src(const rsb_mat *T, int kind) {
     const bool unit = (kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T_UNIT);
     const bool is_dot = (kind == RSB_TRI_LOWER_T || kind == RSB_TRI_LOWER_T_UNIT || kind == RSB_TRI_UPPER_T);
     const bool lower = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T ||
                         kind == RSB_TRI_LOWER_T_UNIT);
-    const bool forward = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_UPPER_T);
     TaskSrc s{};
+    s.forward = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_UPPER_T) ? 1 : 0;
     if (is_dot) {  // task j = column j, rows as stored; the diagonal first (lower) / last (upper)
         s.ptr = T->c_ptr;
         s.idx = T->c_idx;
@@ -456,6 +436,87 @@ int tri_analyse_device(rsb_mat *T, int kind, TriSched **out) {
         s.last_off = (!unit && lower) ? 1 : 0;    // lower rows: the diagonal comes last
         s.diag_at = unit ? -1 : (lower ? 1 : 0);
     }
+    return s;
+}
+
+namespace {
+// dependencies closer than `near` positions, and the longest line (diagonal included)
+__global__ void kd_nat_stats(TaskSrc s, int n, int64_t near, unsigned long long *cnt, int *max_line) {
+    unsigned long long c = 0;
+    int ml = 0;
+    GRID_STRIDE(t64, n) {
+        const int t = (int)t64;
+        int64_t base;
+        int len;
+        s.task(t, base, len);
+        ml = max(ml, s.ptr[t + 1] - s.ptr[t]);
+        for (int k = 0; k < len; ++k) {
+            const int64_t d = (int64_t)s.idx[base + (int64_t)s.step * k] - t;
+            c += (d < 0 ? -d : d) < near;
+        }
+    }
+    if (c) atomicAdd(cnt, c);
+    atomicMax(max_line, ml);
+}
+}  // namespace
+
+// Decide whether a wide schedule runs the index-order kernel (trsv_nat.cu).
+// A dependency closer than the tasks in flight (~kNatNear) may make its
+// consumer wait; with fewer than one such dependency per task on average the
+// waiting chains stay short (config 4 at n = 8e6: 0.4 - 0.8), while a banded
+// matrix (every dependency near) would serialise, and keeps the level order.
+int tri_setup_nat(rsb_mat *T, int kind, TriSched *S) {
+    S->use_nat = false;
+    if (!S->wide || S->n == 0) return RSB_OK;
+    const char *oe = getenv("RSB_TRSV_ORDER");
+    if (oe && std::strcmp(oe, "level") == 0) return RSB_OK;
+    const bool force = oe && std::strcmp(oe, "natural") == 0;
+    rsb_ctx *ctx = T->ctx;
+    cudaStream_t st = ctx->stream;
+    const TaskSrc s = tri_task_src(T, kind);
+    Scratch sc(ctx);
+    unsigned long long *cnt = nullptr;
+    int *ml = nullptr;
+    RSB_TRY(sc.get(&cnt, 1));
+    RSB_TRY(sc.get(&ml, 1));
+    RSB_TRY_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    RSB_TRY_CUDA(cudaMemsetAsync(ml, 0, sizeof(int), st));
+    kd_nat_stats<<<blocks_for(S->n), kT, 0, st>>>(s, S->n, kNatNear, cnt, ml);
+    RSB_TRY_CUDA(cudaGetLastError());
+    unsigned long long h_cnt = 0;
+    int h_ml = 0;
+    RSB_TRY_CUDA(cudaMemcpyAsync(&h_cnt, cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, st));
+    RSB_TRY_CUDA(cudaMemcpyAsync(&h_ml, ml, sizeof h_ml, cudaMemcpyDeviceToHost, st));
+    RSB_TRY_CUDA(cudaStreamSynchronize(st));
+    S->nat = s;
+    S->nat_near = (int64_t)h_cnt;
+    // window: 1.25 x the mean slice span + slack, at least the longest line
+    const int64_t mean32 = 32 * T->nnz / std::max<int64_t>(1, S->n);
+    int64_t cap = (mean32 * 5 / 4 + 48 + 31) / 32 * 32;
+    cap = std::max<int64_t>(cap, ((int64_t)h_ml + 31) / 32 * 32);
+    cap = std::max<int64_t>(cap, 96);
+    if (const char *ce = getenv("RSB_NAT_CAP")) cap = std::max<int64_t>(((int64_t)h_ml + 31) / 32 * 32, atoi(ce));
+    if (cap > kNatMaxCap) return RSB_OK;  // a line too long for the window: level order
+    S->nat_cap = (int32_t)cap;
+    S->use_nat = force || (int64_t)h_cnt < (int64_t)S->n;
+    if (getenv("RSB_DEBUG_ANALYSIS"))
+        fprintf(stderr, "[rsb] index-order solve kind=%d n=%d near=%lld max_line=%d cap=%d use=%d\n", kind, S->n,
+                (long long)h_cnt, h_ml, (int)cap, (int)S->use_nat);
+    return RSB_OK;
+}
+
+// Level analysis of a wide schedule on the device (n > kCtaTriMaxN: never
+// single-CTA).  Produces analysis.cpp's grid schedule.
+int tri_analyse_device(rsb_mat *T, int kind, TriSched **out) {
+    rsb_ctx *ctx = T->ctx;
+    cudaStream_t st = ctx->stream;
+    const int n = (int)T->ncols;
+    const bool unit = (kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T_UNIT);
+    const bool is_dot = (kind == RSB_TRI_LOWER_T || kind == RSB_TRI_LOWER_T_UNIT || kind == RSB_TRI_UPPER_T);
+    const bool lower = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_LOWER_T ||
+                        kind == RSB_TRI_LOWER_T_UNIT);
+    const bool forward = (kind == RSB_TRI_LOWER || kind == RSB_TRI_LOWER_UNIT || kind == RSB_TRI_UPPER_T);
+    const TaskSrc s = tri_task_src(T, kind);
     Scratch sc(ctx);
     int *chk = nullptr;
     RSB_TRY(sc.get(&chk, 4));

@@ -1038,7 +1038,9 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
 __global__ void __launch_bounds__(kBlock) k_band_prod(Banded B, int64_t nnz, VecIn y, Gate g) {
     if (gated(g)) return;
     const int64_t e = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-    if (e < nnz) B.prod[e] = __dmul_rn(__ldcs(B.val + e), vin(y, __ldcs(B.idx + e)));
+    // the products stream out (768 MB at config 4, read back once by the sum
+    // pass): evict-first, so that the band of y stays in L2
+    if (e < nnz) __stcs(B.prod + e, __dmul_rn(__ldcs(B.val + e), vin(y, __ldcs(B.idx + e))));
 }
 
 struct BandTerm {
@@ -1074,6 +1076,68 @@ __global__ void __launch_bounds__(kBlock) k_band_sum(Banded B, int32_t ncols, do
     z[j] = acc;
 }
 
+// Tiled sum pass: a block owns kBlock consecutive columns; their products of
+// band b are one contiguous run of the band-major array, staged into shared
+// memory with coalesced loads (the per-column segments read straight from
+// HBM are ~24-byte pieces: k_band_sum measured 2.17 ms for A^T y at config 4).
+constexpr int kBandCap = 4608;  // staged products per tile (2 x 36 KB): 18 per column
+template <int EPI>
+__global__ void __launch_bounds__(kBlock) k_band_sum_tile(Banded B, int32_t ncols, double *z, VecIn e, Gate g) {
+    if (gated(g)) return;
+    extern __shared__ double band_smem[];
+    double *sp = band_smem;            // band-major, as loaded
+    double *sq = band_smem + kBandCap; // column-major: each column's products in entry order
+    const int64_t l0 = blockIdx.x * (int64_t)kBlock;
+    const int64_t lend = min((int64_t)ncols, l0 + kBlock);
+    const int64_t j = l0 + threadIdx.x;
+    const bool valid = j < ncols;
+    // band b of the tile: global run [g0[b], g0[b] + cnt), staged at sp + off[b]
+    int off = 0, start = 0, n = 0;
+    int my_lo[kMaxBands], my_cnt[kMaxBands], my_off[kMaxBands];
+#pragma unroll
+    for (int b = 0; b < kMaxBands; ++b) {
+        my_lo[b] = my_cnt[b] = my_off[b] = 0;
+        if (b < B.nbands) {
+            const int32_t *bp = B.bptr[b];
+            const int g0 = bp[l0], g1 = bp[lend];
+            if (valid) {
+                my_lo[b] = bp[j];
+                my_cnt[b] = bp[j + 1] - my_lo[b];
+            }
+            my_off[b] = off + (my_lo[b] - g0);
+            start += valid ? my_lo[b] - g0 : 0;
+            n += my_cnt[b];
+            if (off + (g1 - g0) <= kBandCap)
+                for (int i = threadIdx.x; i < g1 - g0; i += kBlock) sp[off + i] = __ldcs(B.prod + g0 + i);
+            off += g1 - g0;
+        }
+    }
+    const bool staged = off <= kBandCap;  // uniform over the block
+    double acc = 0.0;
+    if (staged) {
+        __syncthreads();
+        int pos = start;
+#pragma unroll
+        for (int b = 0; b < kMaxBands; ++b)
+            if (b < B.nbands)
+                for (int k = 0; k < my_cnt[b]; ++k) sq[pos++] = sp[my_off[b] + k];
+        if (n > 0) acc = __dadd_rn(sq[start], pw_smem(sq + start + 1, n - 1));
+    } else if (valid) {  // a tile past the staging buffer: straight from the band-major array
+        BandTerm t;
+        t.prod = B.prod;
+        t.nb = B.nbands;
+#pragma unroll
+        for (int b = 0; b < kMaxBands; ++b) {
+            t.lo[b] = my_lo[b];
+            t.cnt[b] = my_cnt[b];
+        }
+        if (n > 0) acc = __dadd_rn(t(0), n - 1 <= 128 ? pw_leaf(t, 1, n - 1) : Pairwise<25, BandTerm>::sum(t, 1, n - 1));
+    }
+    if (!valid) return;
+    if (EPI == EPI_ADD) acc = __dadd_rn(vin(e, j), acc);
+    z[j] = acc;
+}
+
 int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
     if (At.nlines == 0) return RSB_OK;
     const int grid = grid_for(At.nlines, kBlock);
@@ -1084,10 +1148,25 @@ int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int ep
         const Banded B = *At.bands;
         k_band_prod<<<(unsigned)((At.nnz + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(B, At.nnz, y, g);
         RSB_TRY(post_launch(ctx));
-        if (epi == EPI_ADD)
-            k_band_sum<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
-        else
-            k_band_sum<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
+        static const bool flat = getenv("RSB_BANDS_FLAT") && atoi(getenv("RSB_BANDS_FLAT")) != 0;  // experiments
+        if (flat) {
+            if (epi == EPI_ADD)
+                k_band_sum<EPI_ADD><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
+            else
+                k_band_sum<EPI_STORE><<<grid, kBlock, 0, ctx->stream>>>(B, At.nlines, z, e, g);
+        } else {
+            constexpr size_t smem = 2 * kBandCap * sizeof(double);
+            static bool attr = false;
+            if (!attr) {
+                RSB_TRY_CUDA(cudaFuncSetAttribute(k_band_sum_tile<EPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                RSB_TRY_CUDA(cudaFuncSetAttribute(k_band_sum_tile<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr = true;
+            }
+            if (epi == EPI_ADD)
+                k_band_sum_tile<EPI_ADD><<<grid, kBlock, smem, ctx->stream>>>(B, At.nlines, z, e, g);
+            else
+                k_band_sum_tile<EPI_STORE><<<grid, kBlock, smem, ctx->stream>>>(B, At.nlines, z, e, g);
+        }
         return post_launch(ctx);
     }
     if (spmv_tiled()) {
@@ -1164,6 +1243,9 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         }
     } else if (T.lsync) {
         RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
+    } else if (T.wide && T.use_nat) {
+        RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
+        RSB_TRY(launch_trsv_nat(ctx, T, v, a, c, x, g));  // sentinel fill, then the solve (counted below)
     } else if (T.wide && T.level_sync) {
         // level-synchronous cooperative solve (trsv_ls.cu), the default for wide DAGs
         RSB_TRY(launch_trsv_ls(ctx, T, v, a, c, x, reinterpret_cast<unsigned *>(v.ticket), g, 1, nullptr, 0));

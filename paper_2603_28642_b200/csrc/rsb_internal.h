@@ -147,6 +147,24 @@ struct Gate {
     const int *b;
 };
 
+// Task t's entries in the reference's accumulation order, read from the
+// matrix's own arrays: idx/val[base + step * k], k < len (column t of the CSC
+// for the transposed solves, row t of the CSR -- columns ascending /
+// descending -- otherwise; the diagonal excluded for the non-unit kinds).
+struct TaskSrc {
+    const int32_t *ptr, *idx;
+    const double *val;
+    int first_off, last_off, step;  // base = ptr[t] + first_off (step +1) or ptr[t+1] - 1 - last_off (step -1)
+    int diag_at;                    // 0: ptr[t] (first), 1: ptr[t+1] - 1 (last), -1: unit
+    int forward;                    // dependency order: t ascending (1) or descending (0)
+    __device__ void task(int t, int64_t &base, int &len) const {
+        const int lo = ptr[t], hi = ptr[t + 1];
+        len = (hi - lo) - first_off - last_off;
+        base = step > 0 ? (int64_t)lo + first_off : (int64_t)hi - 1 - last_off;
+    }
+};
+using NatSrc = TaskSrc;
+
 // Level-ordered triangular-solve schedule: task t solves unknown task_row[t];
 // tasks are sorted by dependency level, so every dependency of task t is a task
 // < t.  Warp slice w (tasks 32w..32w+31) stores its entries interleaved --
@@ -254,6 +272,12 @@ struct TriSched {
     bool wide_static = false;
     int32_t static_n = 4;
     bool wide = false;
+    // index-order sync-free kernel (trsv_nat.cu) reading the matrix's own
+    // arrays: chosen when few dependencies are near in index distance
+    bool use_nat = false;
+    NatSrc nat{};
+    int32_t nat_cap = 0;      // entries of a warp's shared-memory window (>= the longest line)
+    int64_t nat_near = 0;     // dependencies closer than kNatNear positions
     // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
     bool lsync = false;
     // wide DAGs: one cooperative kernel walking the levels with grid barriers
@@ -380,6 +404,14 @@ int prepare_trsv_cta(int64_t n);
 int prepare_trsv_lean(int64_t smem_bytes);
 int launch_trsv_lean(rsb_ctx *ctx, const TriSched &T, const TriDev &v, double *x, Gate g);
 int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g);
+// index-order sync-free solve (trsv_nat.cu); tri_setup_nat decides whether a
+// wide schedule uses it (RSB_TRSV_ORDER=natural | level overrides)
+constexpr int64_t kNatNear = 1 << 18;
+constexpr int kNatMaxCap = 1024;
+int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g);
+size_t trsv_nat_smem(int mode, int cap);
+int tri_setup_nat(rsb_mat *T, int kind, TriSched *S);
+TaskSrc tri_task_src(const rsb_mat *T, int kind);
 // level-synchronous cooperative solve of a wide schedule for nb = 1 or 8
 // interleaved right-hand sides (rstat: per-RHS status words, stride in ints)
 int launch_trsv_ls(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x,

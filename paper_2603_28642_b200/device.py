@@ -190,7 +190,7 @@ class DeviceMatrix:
         """(kernel family, longest task of the lean kernel or 0) of a solve."""
         v, n = ctypes.c_int(), ctypes.c_int()
         L.check(L.lib().rsb_trsv_variant(self.h, kind, ctypes.byref(v), ctypes.byref(n)))
-        return ("grid", "staged", "lean", "levels", "lsync", "levelsync")[v.value], n.value
+        return ("grid", "staged", "lean", "levels", "lsync", "levelsync", "natural")[v.value], n.value
 
     def levels(self, kind: int):
         nl, mw = ctypes.c_int64(), ctypes.c_int64()

@@ -106,6 +106,26 @@ def test_config4_structure_batch(mode):
         assert _same_report(reports[j], repo), f"rhs {j}: report differs"
 
 
+@pytest.mark.parametrize("order", ["natural", "level"])
+def test_config4_structure_solve_order(order, monkeypatch):
+    """The same structure with the wide solves forced to the index-order
+    kernel (trsv_nat.cu; the default at n = 8e6, where dependencies are far)
+    and to the level-ordered one: both bit-identical to the oracle."""
+    from paper_2603_28642_b200 import _lib as L
+    from paper_2603_28642_b200 import device
+
+    monkeypatch.setenv("RSB_TRSV_ORDER", order)
+    device.clear_caches()
+    A, B = W.config4(seed=4, n=200_000, nrhs=1)
+    S, na, f = _pipeline(A, True, 1.0, 0.0, 4)
+    want = "natural" if order == "natural" else "grid"
+    for M, kind in ((f.L1, L.TRI_LOWER_UNIT), (f.L1, L.TRI_LOWER_T_UNIT), (f.U, L.TRI_UPPER)):
+        Mc = P.CscMatrix(M.nrows, M.ncols, M.col_ptr, M.row_idx, M.values)
+        assert device.DeviceMatrix(Mc, device.get_context()).variant(kind)[0] == want
+    _check(S, B[0], na, f, "cg", 1e-300, 6, 4)
+    device.clear_caches()
+
+
 def test_config4_structure_fixed_iterations_wide_dag():
     """configs[4] structure at n = 200,000 (wide DAGs: the grid-wide
     sync-free solve) for a fixed 6 iterations (delta = 1e-300, the bench's

@@ -142,7 +142,8 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
 
 
 @pytest.mark.parametrize("grid", ["levelsync", "levelsync-n4", "lsync", "syncfree", "syncfree-pairs",
-                                  "syncfree-unsorted", "syncfree-n4", "static", "static-n4"])
+                                  "syncfree-unsorted", "syncfree-n4", "static", "static-n4", "natural",
+                                  "natural-cap32", "natural-minb6", "natural-static"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -159,6 +160,16 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
         monkeypatch.setenv("RSB_TRSV_GRID", "syncfree")
     if grid == "static-n4":
         monkeypatch.setenv("RSB_WIDE_N", "4")
+    if grid.startswith("natural"):  # index-order kernel (trsv_nat.cu) reading the matrix's own arrays
+        monkeypatch.setenv("RSB_TRSV_ORDER", "natural")
+    else:
+        monkeypatch.setenv("RSB_TRSV_ORDER", "level")
+    if grid == "natural-cap32":  # the smallest window: every slice takes several passes
+        monkeypatch.setenv("RSB_NAT_CAP", "32")
+    if grid.startswith("natural-minb"):
+        monkeypatch.setenv("RSB_NAT_MINB", grid[-1])
+    if grid == "natural-static":  # round-robin slices under a cooperative launch instead of the ticket
+        monkeypatch.setenv("RSB_NAT_STATIC", "1")
     if grid == "levelsync-n4":  # level-synchronous with 4 register entries: long tasks take the tail
         monkeypatch.setenv("RSB_WIDE_N", "4")
     if grid == "syncfree-pairs":
@@ -181,7 +192,8 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     U = transpose(M)
     for kind in (L.TRI_UPPER, L.TRI_UPPER_T):
         check(U, kind, b, monkeypatch)
-    want = {"lsync": "lsync", "levelsync": "levelsync", "levelsync-n4": "levelsync"}.get(grid, "grid")
+    want = {"lsync": "lsync", "levelsync": "levelsync", "levelsync-n4": "levelsync"}.get(
+        grid, "natural" if grid.startswith("natural") else "grid")
     assert variant(M, L.TRI_LOWER)[0] == want
 
 
