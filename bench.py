@@ -266,18 +266,41 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload_key):
-    """DRAM bytes (read + write) per iteration of the dominant kernel class
-    from the committed ncu capture of this workload, or (None, why)."""
+def ncu_traffic(workload_key, cls):
+    """DRAM bytes (read + write) per iteration of a kernel class ("solves" |
+    "products") from the committed ncu capture of this workload
+    (scripts/ncu_traffic.py), or (None, why)."""
     path = os.path.join(HERE, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             d = json.load(fh).get(workload_key)
-        if d:
-            return d.get("dram_bytes_per_iteration"), d.get("source")
+        if d and cls in d:
+            return d[cls].get("dram_bytes_per_iteration"), d[cls].get("source")
     except (OSError, ValueError):
         pass
     return None, "no ncu capture committed for this workload"
+
+
+def spmv_bytes(nnz, rows, cols):
+    """int32 indices, f64 values, every operand once."""
+    return 12 * nnz + 4 * (rows + 1) + 8 * cols + 8 * rows
+
+
+def product_bytes_per_iteration(S, f, mode, cg_iters=2):
+    """Algorithmic bytes of the sparse products of one iteration: A p, A^T r
+    (sv.py:209,234) and the L2 / L2^T products of the apply (pc.py:135-186)."""
+    a = spmv_bytes(S.nnz, S.nrows, S.ncols)
+    s, n = f.L2.nrows, f.L2.ncols
+    l2 = spmv_bytes(f.L2.nnz, s, n)
+    if s == 0:
+        counts = {"A_x": 1, "AT_y": 1, "L2_t": 0, "L2T_w": 0}
+    elif mode == "cg":
+        counts = {"A_x": 1, "AT_y": 1, "L2_t": 1 + cg_iters, "L2T_w": 1 + cg_iters}
+    elif mode == "identity":
+        counts = {"A_x": 1, "AT_y": 1, "L2_t": 1, "L2T_w": 1}
+    else:  # dense: the explicit Y takes the place of L2 (its own size is not counted here)
+        return 2 * a, {"A_x": 1, "AT_y": 1, "L2_t": 0, "L2T_w": 0}
+    return 2 * a + (counts["L2_t"] + counts["L2T_w"]) * l2, counts
 
 
 def host_cpu():
@@ -475,6 +498,9 @@ def run_b200(args):
         raise RuntimeError(f"solver left the fixed-iteration run early (status {st_c[0]})")
     iter_ms_max = barrier_max(float(it_ms[0]))
     value = world * K / (iter_ms_max / 1e3)
+    prod_ms, prod_launches = np.zeros(1), np.zeros(1, dtype=np.int64)
+    L.check(L.lib().rsb_solver_bench_products(solver.h, prod_ms.ctypes.data_as(L.f64p),
+                                              prod_launches.ctypes.data_as(L.i64p)))
 
     # ---- end to end through the public API (host buffers, copies inside)
     bpin = D.PinnedBuffer(len(b))
@@ -548,12 +574,29 @@ def run_b200(args):
         if dist is not None:
             dist[1].destroy_process_group()
         return
-    # ---- roofline of the dominant kernel class (the triangular solves)
-    tbytes, counts = trsv_bytes_per_iteration(f, mode)
-    achieved = (tbytes * K) / (tri_ms[0] / 1e3) / 1e9
+    # ---- roofline of the dominant kernel class: the triangular solves or the
+    # sparse products, whichever took more of the timed iterations (both
+    # classes are reported; event pairs around every launch of the class)
     peak, peak_kind = measured_peak()
     wkey = f"config{args.config}_n{S.ncols}_mu{args.mu}_{mode}"
-    traffic, traffic_src = ncu_traffic(wkey)
+    tbytes, counts = trsv_bytes_per_iteration(f, mode)
+    pbytes, pcounts = product_bytes_per_iteration(S, f, mode)
+    classes = {}
+    for cls, label, by, cnt, ms in (
+            ("solves", "sparse triangular solves", tbytes, counts, float(tri_ms[0])),
+            ("products", "sparse products (A x, A^T y, L2 t, L2^T w)", pbytes, pcounts, float(prod_ms[0]))):
+        tr, tr_src = ncu_traffic(wkey, cls)
+        ach = (by * K) / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        classes[cls] = {"kernel": f"{label}, {sum(cnt.values())} per iteration ({cnt})", "bound": "hbm",
+                        "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_kind": peak_kind,
+                        "traffic": tr, "traffic_source": tr_src, "algorithmic_bytes_per_iteration": by,
+                        "ms_per_iteration": ms / K, "share_of_step": ms / float(it_ms[0])}
+    dom = max(classes, key=lambda c: classes[c]["ms_per_iteration"])
+    roofline = dict(classes[dom])
+    roofline["other_class"] = {c: v for c, v in classes.items() if c != dom}
+    roofline["note"] = ("classes overlap in time: A^T r runs on a side branch concurrently with the preconditioner "
+                        "application, so the shares can sum past 1; random 8-byte gathers are bounded by the L1TEX "
+                        "wavefront rate, not by HBM (DESIGN.md section 5)")
     model, cores = host_cpu()
 
     # ---- parity against the oracle port + the CPU baseline (rank 0, N = 1)
@@ -615,15 +658,7 @@ def run_b200(args):
                   if not args.no_flush else "not flushed",
             "parallelism": f"replicas x{world}",
         },
-        "roofline": {
-            "kernel": f"sparse triangular solves, {sum(counts.values())} per iteration ({counts})",
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
-            "traffic_source": traffic_src,
-            "algorithmic_bytes_per_iteration": tbytes,
-            "share_of_step": float(tri_ms[0] / it_ms[0]),
-            "iteration_gbs_algorithmic": None,
-        },
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "parity": parity,
         "e2e": {"value": e2e, "unit": "iter/s", "h2d_bytes_per_step": 8 * S.nrows / K,

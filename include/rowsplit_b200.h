@@ -213,6 +213,10 @@ int rsb_solver_finish(rsb_solver *S, rsb_report *rep, double *history, int64_t h
  * device ms of the iterations and of the triangular solves inside them. */
 int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, double *tri_ms,
                      int64_t *tri_launches, int64_t *kernels_per_iter, int *status);
+/* the sparse products (A x, A^T y, L2 t, L2^T w; sc.py:212-235) of the last
+ * rsb_solver_bench call: their summed device ms (A^T r runs on a side branch
+ * concurrently with the preconditioner, so classes can overlap) and count */
+int rsb_solver_bench_products(rsb_solver *S, double *prod_ms, int64_t *prod_launches);
 /* overwrite a 320 MiB scratch buffer (> L2) on the context stream */
 int rsb_l2_flush(rsb_ctx *ctx);
 /* whole solve in one call: start + iterate + finish + get_x */

@@ -91,6 +91,7 @@ _SIGS = {
     "rsb_pcgls_many": [ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(CglsCfgC),
                        ctypes.POINTER(vp), ctypes.POINTER(ReportC), vp, i64],
     "rsb_solver_bench": [vp, i64, ctypes.c_int, f64p, f64p, i64p, i64p, ctypes.POINTER(ctypes.c_int)],
+    "rsb_solver_bench_products": [vp, f64p, i64p],
     "rsb_l2_flush": [vp],
     "rsb_bsolver_create": [vp, vp, ctypes.POINTER(vp)],
     "rsb_bsolver_destroy": [vp],

@@ -162,6 +162,7 @@ int rsb_ctx_create(int device, int flags, rsb_ctx **out) {
     for (int i = 0; e == cudaSuccess && i < 3; ++i) e = cudaEventCreateWithFlags(&ctx->fork_ev[i], cudaEventDisableTiming);
     for (int i = 0; e == cudaSuccess && i < 16; ++i) e = cudaEventCreate(&ctx->ev[i]);
     for (int i = 0; e == cudaSuccess && i < 64; ++i) e = cudaEventCreate(&ctx->trace_ev[i]);
+    for (int i = 0; e == cudaSuccess && i < 64; ++i) e = cudaEventCreate(&ctx->ptrace_ev[i]);
     if (e == cudaSuccess) e = cudaMallocHost((void **)&ctx->h_scalar, 64 * sizeof(double));
     if (e != cudaSuccess) {
         set_error("context setup failed: %s", cudaGetErrorString(e));
@@ -201,6 +202,8 @@ int rsb_ctx_destroy(rsb_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : ctx->trace_ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : ctx->ptrace_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->flush_buf) dev_free(ctx, ctx->flush_buf, ctx->flush_bytes);
     for (auto &e : ctx->fork_ev)

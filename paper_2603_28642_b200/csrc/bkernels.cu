@@ -163,6 +163,7 @@ __device__ __noinline__ double bline_pw(const Compressed &A, const VecIn &y, int
 // runs the per-line code instead.
 constexpr int kBTile = 32;
 constexpr int kBTileCap = 512;
+constexpr int kBTileRounds = 1;
 
 template <bool TRANS>
 struct BTerm {
@@ -171,8 +172,12 @@ struct BTerm {
     __device__ double operator()(int64_t k) const { return p[k * kB + r]; }
 };
 
-template <bool TRANS, int EPI>
-__global__ void __launch_bounds__(kBlk, 3) kb_spmv_tile(Compressed A, VecIn x, double *y, VecIn e, const int *all_done) {
+// ROUNDS: the tile's products are formed in ROUNDS passes of kBTileCap /
+// kBTile / ROUNDS entries per octet (1: 16 gathers in flight per thread, 80
+// registers, 3 blocks per SM; 2: 8 in flight, more resident blocks)
+template <bool TRANS, int EPI, int ROUNDS>
+__global__ void __launch_bounds__(kBlk, ROUNDS == 1 ? 3 : 5) kb_spmv_tile(Compressed A, VecIn x, double *y, VecIn e,
+                                                                        const int *all_done) {
     if (all_off(all_done)) return;
     __shared__ double prod[kBTileCap * kB];
     const int oct = threadIdx.x >> 3, r = threadIdx.x & 7;
@@ -183,20 +188,24 @@ __global__ void __launch_bounds__(kBlk, 3) kb_spmv_tile(Compressed A, VecIn x, d
     const int lo = A.ptr[l0], hi = A.ptr[lend];
     double acc = 0.0;
     if (hi - lo <= kBTileCap) {
-        constexpr int U = kBTileCap / kBTile;
-        int c[U];
-        double v[U], xv[U];
+        constexpr int U = kBTileCap / kBTile / ROUNDS;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int k = lo + oct + kBTile * u;
-            c[u] = k < hi ? __ldcs(A.idx + k) : -1;
-            v[u] = k < hi ? __ldcs(A.val + k) : 0.0;
+        for (int h = 0; h < ROUNDS; ++h) {
+            if (h > 0 && lo + kBTile * U * h >= hi) break;
+            int c[U];
+            double v[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = lo + oct + kBTile * (u + U * h);
+                c[u] = k < hi ? __ldcs(A.idx + k) : -1;
+                v[u] = k < hi ? __ldcs(A.val + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? x.p[bidx(x, c[u]) * kB + r] : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (c[u] >= 0) prod[(oct + kBTile * (u + U * h)) * kB + r] = __dmul_rn(v[u], xv[u]);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? x.p[bidx(x, c[u]) * kB + r] : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (c[u] >= 0) prod[(oct + kBTile * u) * kB + r] = __dmul_rn(v[u], xv[u]);
         __syncthreads();
         if (!valid) return;
         const int s0 = A.ptr[i] - lo, t0 = A.ptr[i + 1] - lo;
@@ -237,6 +246,11 @@ __global__ void __launch_bounds__(kBlk) kb_spmv_rows(Compressed A, VecIn x, doub
     if (EPI == EPI_SUB_FROM) acc = __dsub_rn(e.p[bidx(e, i) * kB + r], acc);
     y[i * kB + r] = acc;
 }
+
+// (CSC products with an octet of lanes per column straight from global
+// memory, the CSR kernel's scheme, measured far slower than the tiled kernel:
+// 87 vs 36.5 ms per batched iteration at n = 8e6 -- a column's pairwise order
+// needs its products 8 at a time, two dependent round trips per column.)
 
 // ---- a @ b per RHS in the context's OpenBLAS order.  Block = 256 threads:
 // thread t runs accumulator chain t >> 3 (of the 32 the OpenBLAS kernel
@@ -509,14 +523,19 @@ __device__ __forceinline__ void st_flag_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// 4 consecutive doubles (16-byte aligned), through L2
+// 4 consecutive doubles (32-byte aligned: half of a 64-byte row), through L2,
+// as ONE 256-bit load (sm_100 LDG.256): a warp whose lanes read 32 different
+// rows pays 32 L1TEX wavefronts per load instruction, so two 16-byte loads per
+// half cost twice the wavefronts for the same bytes
 __device__ __forceinline__ void ld4(const double *p, double (&v)[4]) {
-    const double2 a = __ldcg(reinterpret_cast<const double2 *>(p));
-    const double2 b = __ldcg(reinterpret_cast<const double2 *>(p) + 1);
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = b.x;
-    v[3] = b.y;
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void st4(double *p, const double (&v)[4]) {
+    asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
 }
 
 // entries of the task past `from` (contiguous, then -1 padding)
@@ -681,9 +700,7 @@ __global__ void __launch_bounds__(kBlk, 2) kb_trsv(TriDev T, VecIn a, const doub
                             if ((MODE & 1) && len > 0) acc[q] = __dsub_rn(acc[q], dot[q]);
                             if (MODE & 2) acc[q] = __ddiv_rn(acc[q], d);
                         }
-                        double2 *o = reinterpret_cast<double2 *>(x + (int64_t)row * kB + 4 * h);
-                        __stcg(o, make_double2(acc[0], acc[1]));
-                        __stcg(o + 1, make_double2(acc[2], acc[3]));
+                        st4(x + (int64_t)row * kB + 4 * h, acc);
                     }
                     st_flag_release(flag + row, E);
                     done = true;
@@ -859,9 +876,7 @@ __global__ void __launch_bounds__(kBlk, 2) kb_trsv_static(TriDev T, VecIn a, con
                             if ((MODE & 1) && len > 0) ah[q] = __dsub_rn(ah[q], dot[q]);
                             if (MODE & 2) ah[q] = __ddiv_rn(ah[q], cur.d);
                         }
-                        double2 *o = reinterpret_cast<double2 *>(x + (int64_t)cur.row * kB + 4 * h);
-                        __stcg(o, make_double2(ah[0], ah[1]));
-                        __stcg(o + 1, make_double2(ah[2], ah[3]));
+                        st4(x + (int64_t)cur.row * kB + 4 * h, ah);
                     }
                     st_flag_release(flag + cur.row, E);
                     done = true;
@@ -939,10 +954,17 @@ int launch_bspmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi,
 int launch_bspmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, const int *all_done) {
     if (At.nlines == 0) return RSB_OK;
     const int grid = (int)((At.nlines + kBTile - 1) / kBTile);
-    if (epi == EPI_ADD)
-        kb_spmv_tile<true, EPI_ADD><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+    const char *er = getenv("RSB_BTILE_ROUNDS");  // experiments
+    const int rounds = er ? atoi(er) : kBTileRounds;
+    if (rounds == 2) {
+        if (epi == EPI_ADD)
+            kb_spmv_tile<true, EPI_ADD, 2><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+        else
+            kb_spmv_tile<true, EPI_STORE, 2><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+    } else if (epi == EPI_ADD)
+        kb_spmv_tile<true, EPI_ADD, 1><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
     else
-        kb_spmv_tile<true, EPI_STORE><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+        kb_spmv_tile<true, EPI_STORE, 1><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
     return bpost(ctx);
 }
 
@@ -1027,6 +1049,12 @@ int launch_btrsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doub
     kb_bump<<<1, 1, 0, ctx->stream>>>(ws.epoch);
     RSB_TRY(bpost(ctx));
     RSB_TRY_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned long long), ctx->stream));
+    if (btrsv_nat_supported(T)) {
+        RSB_TRY(launch_btrsv_nat(ctx, T, a, c, x, ws, all_done));
+        if (trace)
+            RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
+        return RSB_OK;
+    }
     const int32_t lvl1 = T.h_level_ptr.size() > 1 ? T.h_level_ptr[1] : T.n;
     if (lvl1 > 0) {
         const int g0 = grid_stride_n((int64_t)lvl1 * kB);

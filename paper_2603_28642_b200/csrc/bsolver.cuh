@@ -55,6 +55,10 @@ int launch_bunpack(rsb_ctx *ctx, double *dst, const double *src, int64_t len, in
 bool btrsv_supported(const TriSched &T);
 int launch_btrsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, BTriWs &ws,
                  const int *all_done);
+// index-order batched solve (btrsv_nat.cu), for schedules the analysis gave the index order
+bool btrsv_nat_supported(const TriSched &T);
+int launch_btrsv_nat(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, BTriWs &ws,
+                     const int *all_done);
 int bpost(rsb_ctx *ctx);
 
 }  // namespace rsb

@@ -490,6 +490,7 @@ int tri_setup_nat(rsb_mat *T, int kind, TriSched *S) {
     RSB_TRY_CUDA(cudaStreamSynchronize(st));
     S->nat = s;
     S->nat_near = (int64_t)h_cnt;
+    S->nat_max_line = h_ml;
     // window: 1.25 x the mean slice span + slack, at least the longest line
     const int64_t mean32 = 32 * T->nnz / std::max<int64_t>(1, S->n);
     int64_t cap = (mean32 * 5 / 4 + 48 + 31) / 32 * 32;

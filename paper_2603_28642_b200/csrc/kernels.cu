@@ -1003,7 +1003,7 @@ static int spmv_force() {
 }
 static bool spmv_tiled() { return spmv_force() != 1; }
 
-int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
+static int spmv_impl(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
     if (A.nlines == 0) return RSB_OK;
     const int grid = grid_for(A.nlines, kBlock);
     // rows of at most 8 entries (A of configs 0 / 4: 6 per row): one thread per
@@ -1138,7 +1138,7 @@ __global__ void __launch_bounds__(kBlock) k_band_sum_tile(Banded B, int32_t ncol
     z[j] = acc;
 }
 
-int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
+static int spmv_t_impl(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
     if (At.nlines == 0) return RSB_OK;
     const int grid = grid_for(At.nlines, kBlock);
     // the banded path uses the matrix's product scratch: only on the stream of
@@ -1194,6 +1194,27 @@ int launch_fill(rsb_ctx *ctx, double *x, int64_t n, unsigned long long bits, Gat
     if (n == 0) return RSB_OK;
     k_fill<<<grid_stride(n), kBlock, 0, ctx->stream>>>(x, n, bits, g);
     return post_launch(ctx);
+}
+
+// bench instrumentation: event pairs around every sparse product captured
+// into an instrumented iteration graph (on the launching stream)
+template <class F>
+static int traced_product(rsb_ctx *ctx, F &&launch) {
+    const bool trace = ctx->tracing && ctx->ptrace_n + 2 <= 64;
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->ptrace_ev[ctx->ptrace_n++], ctx->stream, cudaEventRecordExternal));
+    RSB_TRY(launch());
+    if (trace)
+        RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->ptrace_ev[ctx->ptrace_n++], ctx->stream, cudaEventRecordExternal));
+    return RSB_OK;
+}
+
+int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, VecIn e, Gate g) {
+    return traced_product(ctx, [&] { return spmv_impl(ctx, A, x, y, epi, e, g); });
+}
+
+int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g) {
+    return traced_product(ctx, [&] { return spmv_t_impl(ctx, At, y, z, epi, e, g); });
 }
 
 int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g,

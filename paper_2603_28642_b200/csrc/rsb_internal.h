@@ -277,6 +277,7 @@ struct TriSched {
     bool use_nat = false;
     NatSrc nat{};
     int32_t nat_cap = 0;      // entries of a warp's shared-memory window (>= the longest line)
+    int32_t nat_max_line = 0; // longest line, diagonal included
     int64_t nat_near = 0;     // dependencies closer than kNatNear positions
     // level-synchronous variant of the wide solve (default for <= kLsMaxLevels levels)
     bool lsync = false;
@@ -344,6 +345,12 @@ struct rsb_ctx {
     bool tracing = false;
     int trace_n = 0;
     cudaEvent_t trace_ev[64] = {};
+    // the same for the sparse products (A x, A^T y, L2 t, L2^T w), recorded on
+    // whichever stream launches them (A^T r runs on the side branch)
+    int ptrace_n = 0;
+    cudaEvent_t ptrace_ev[64] = {};
+    double last_prod_ms = 0.0;  // summed by the last rsb_solver_bench
+    int64_t last_prod_launches = 0;
     // L2 flush buffer (bench only, allocated on first use)
     void *flush_buf = nullptr;
     size_t flush_bytes = 0;

@@ -329,7 +329,7 @@ struct rsb_solver {
     // around every triangular solve
     cudaGraph_t bgraph = nullptr;
     cudaGraphExec_t bexec = nullptr;
-    int btrace = 0;
+    int btrace = 0, bptrace = 0;
     bool started = false;
     rsb_cgls_cfg cfg{};
 };
@@ -881,6 +881,7 @@ int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, doubl
     if (!S->bexec) {
         ctx->tracing = true;
         ctx->trace_n = 0;
+        ctx->ptrace_n = 0;
         const int64_t before = ctx->launches;
         RSB_TRY_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         int rc = enqueue_iteration(S);
@@ -896,8 +897,9 @@ int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, doubl
         S->bgraph = graph;
         RSB_TRY_CUDA(cudaGraphInstantiate(&S->bexec, graph, cudaGraphInstantiateFlagUseNodePriority));
         S->btrace = ctx->trace_n;
+        S->bptrace = ctx->ptrace_n;
     }
-    double it_total = 0.0, tri_total = 0.0;
+    double it_total = 0.0, tri_total = 0.0, prod_total = 0.0;
     for (int64_t i = 0; i < k; ++i) {
         if (flush) RSB_TRY(launch_l2_flush(ctx));
         RSB_TRY_CUDA(cudaEventRecord(ctx->ev[14], ctx->stream));
@@ -912,13 +914,25 @@ int rsb_solver_bench(rsb_solver *S, int64_t k, int flush, double *iter_ms, doubl
             RSB_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->trace_ev[t], ctx->trace_ev[t + 1]));
             tri_total += ms;
         }
+        for (int t = 0; t + 1 < S->bptrace; t += 2) {
+            RSB_TRY_CUDA(cudaEventElapsedTime(&ms, ctx->ptrace_ev[t], ctx->ptrace_ev[t + 1]));
+            prod_total += ms;
+        }
     }
+    ctx->last_prod_ms = prod_total;
+    ctx->last_prod_launches = k * (S->bptrace / 2);
     RSB_TRY(read_state(S));
     *iter_ms = it_total;
     *tri_ms = tri_total;
     *tri_launches = k * (S->btrace / 2);
     *kernels_per_iter = S->graph_kernels;
     *status = S->h_st->status;
+    return RSB_OK;
+}
+
+int rsb_solver_bench_products(rsb_solver *S, double *prod_ms, int64_t *prod_launches) {
+    *prod_ms = S->ctx->last_prod_ms;
+    *prod_launches = S->ctx->last_prod_launches;
     return RSB_OK;
 }
 

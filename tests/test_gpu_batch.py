@@ -131,3 +131,33 @@ def test_batch_static_schedule_option(cfg4, monkeypatch):
     pre2 = P.build_preconditioner(f, s_mode=P.SMode.INNER_CG)
     X1, r1 = P.pcgls_batch(A2, B[:8], pre2, cfg)
     assert np.array_equal(X0, X1) and [_rep(r) for r in r0] == [_rep(r) for r in r1]
+
+
+@pytest.mark.parametrize("mode", ["cg", "identity"])
+def test_batch_index_order_solve(cfg4, mode, monkeypatch):
+    """RSB_TRSV_ORDER=natural + RSB_BTRSV_NAT=1: the index-order batched solve
+    (btrsv_nat.cu, opt-in) against the single solves
+    through the level-ordered kernels, incl. a zero RHS and different stop
+    iterations."""
+    S, B, na, f = cfg4
+    cfg = P.CglsConfig(norm_A=na, delta=1e-8, max_iters=60)
+    Bm = B[:8].copy()
+    Bm[5] = 0.0
+    monkeypatch.setenv("RSB_TRSV_ORDER", "level")
+    D.clear_caches()
+    pre0 = P.build_preconditioner(f, s_mode=P.SMode(mode))
+    singles = _singles(S, Bm, pre0, cfg)
+    monkeypatch.setenv("RSB_TRSV_ORDER", "natural")
+    monkeypatch.setenv("RSB_BTRSV_NAT", "1")
+    D.clear_caches()
+    A2 = P.CscMatrix(S.nrows, S.ncols, S.col_ptr, S.row_idx, S.values)
+    pre = P.build_preconditioner(f, s_mode=P.SMode(mode))
+    from paper_2603_28642_b200 import _lib as L
+
+    dpre = D.device_preconditioner(pre, D.get_context())
+    assert dpre.L1.variant(L.TRI_LOWER_UNIT)[0] == "natural" and dpre.U.variant(L.TRI_UPPER)[0] == "natural"
+    X, reps = P.pcgls_batch(A2, Bm, pre, cfg)
+    for j, (x1, r1) in enumerate(singles):
+        assert np.array_equal(X[j], x1, equal_nan=True), f"rhs {j}: iterate differs"
+        assert _rep(reps[j]) == _rep(r1), f"rhs {j}: report differs"
+    D.clear_caches()
