@@ -163,7 +163,7 @@ __device__ __noinline__ double bline_pw(const Compressed &A, const VecIn &y, int
 // runs the per-line code instead.
 constexpr int kBTile = 32;
 constexpr int kBTileCap = 512;
-constexpr int kBTileRounds = 1;
+constexpr int kBTileRounds = 2;  // measured at n = 8e6: 35.1 -> 32.9 ms per 8-RHS iteration (A^T 3.32 -> 3.03, L2^T -> 2.07 ms)
 
 template <bool TRANS>
 struct BTerm {
@@ -176,7 +176,7 @@ struct BTerm {
 // kBTile / ROUNDS entries per octet (1: 16 gathers in flight per thread, 80
 // registers, 3 blocks per SM; 2: 8 in flight, more resident blocks)
 template <bool TRANS, int EPI, int ROUNDS>
-__global__ void __launch_bounds__(kBlk, ROUNDS == 1 ? 3 : 5) kb_spmv_tile(Compressed A, VecIn x, double *y, VecIn e,
+__global__ void __launch_bounds__(kBlk, ROUNDS == 1 ? 3 : (ROUNDS == 2 ? 5 : 6)) kb_spmv_tile(Compressed A, VecIn x, double *y, VecIn e,
                                                                         const int *all_done) {
     if (all_off(all_done)) return;
     __shared__ double prod[kBTileCap * kB];
@@ -714,6 +714,12 @@ __global__ void __launch_bounds__(kBlk, 2) kb_trsv(TriDev T, VecIn a, const doub
     }
 }
 
+// (A pair variant -- two lanes per task, each carrying 4 right-hand sides, so
+// that the halves of a dependency's row are read by adjacent lanes as one
+// L1TEX wavefront and advance together -- measured slower: 35.4 vs 32.9 ms per
+// 8-RHS iteration at n = 8e6; at 80 registers it spills and holds half as many
+// tasks per warp.)
+
 // Static-schedule batched solve for short-task forward solves (the single-RHS
 // k_trsv_static's scheme): a cooperative launch, warp w owns slices w, w + W,
 // ...; the next slice's row, offsets, entries and right-hand-side index are
@@ -956,7 +962,12 @@ int launch_bspmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int e
     const int grid = (int)((At.nlines + kBTile - 1) / kBTile);
     const char *er = getenv("RSB_BTILE_ROUNDS");  // experiments
     const int rounds = er ? atoi(er) : kBTileRounds;
-    if (rounds == 2) {
+    if (rounds == 4) {
+        if (epi == EPI_ADD)
+            kb_spmv_tile<true, EPI_ADD, 4><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+        else
+            kb_spmv_tile<true, EPI_STORE, 4><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
+    } else if (rounds == 2) {
         if (epi == EPI_ADD)
             kb_spmv_tile<true, EPI_ADD, 2><<<grid, kBlk, 0, ctx->stream>>>(At, y, z, e, all_done);
         else

@@ -369,7 +369,8 @@ int enqueue_iteration(rsb_solver *S) {
     // merely wasted (z is not an output); k_it_zz runs after the join, keeping
     // the reference's order of the stopping checks.  (Not in tree-dot mode,
     // whose dots share one scratch.)
-    const bool fork = !(ctx->flags & RSB_DOT_TREE) && ctx->side;
+    const char *nf = getenv("RSB_NO_FORK");  // experiments: everything on the main branch
+    const bool fork = !(ctx->flags & RSB_DOT_TREE) && ctx->side && !(nf && atoi(nf) != 0);
     auto on_side = [&](auto &&launches) -> int {
         cudaStream_t main = ctx->stream;
         ctx->stream = ctx->side;
