@@ -40,9 +40,10 @@ constexpr int kBnBlock = 128;
 constexpr int kBnWarps = kBnBlock / 32;
 constexpr unsigned kBnMinBackoffNs = 32, kBnMaxBackoffNs = 256;
 
+// acquire polls: a flag seen set orders the row reads after it (no consumer-side fence)
 __device__ __forceinline__ int bn_ld_flag(const int *p) {
     int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void bn_st_flag_release(int *p, int v) {
@@ -151,7 +152,6 @@ __global__ void __launch_bounds__(kBnBlock) kb_trsv_nat(NatSrc s, int n, VecIn a
                     sv[i0 + u * 32] = vi[u];
                 }
             }
-            __threadfence();  // acquire: the flags were seen, now the rows
             __syncwarp();
             // rows of the finished dependencies: four lanes per 64-byte row, every
             // row of the span in flight at once
@@ -260,6 +260,13 @@ __global__ void __launch_bounds__(kBnBlock) kb_trsv_nat(NatSrc s, int n, VecIn a
     }
 }
 
+// (An octet-per-row variant -- the batched CSR product's scheme with flags: rows
+// in index order round-robin over a cooperative launch, no shared memory, each
+// lane of the octet loading and polling one entry of a chunk of 8 -- measured
+// 38.8 ms per 8-RHS iteration at n = 8e6 against 36.0 for the kernel above and
+// 33.0 for the level-ordered one: one release fence per row instead of per
+// 32 rows.)
+
 using BnKernel = void (*)(NatSrc, int, VecIn, const double *, double *, int *, const unsigned *, unsigned long long *,
                           int, const int *);
 
@@ -279,9 +286,10 @@ constexpr int kBnCap = 160;
 }  // namespace
 
 bool btrsv_nat_supported(const TriSched &T) {
-    // opt-in (RSB_BTRSV_NAT=1): per launch it measured 1.66 / 1.33 / 4.30 ms (L1 / L1^T / U at
-    // n = 8e6) against 1.55 / 1.31 / 2.79 for the level-ordered kernel -- 12 warps per SM
-    // (17 KB of shared memory per warp) do not hide the slice's five dependent round trips
+    // opt-in (RSB_BTRSV_NAT=1): 36.0 ms per 8-RHS iteration at n = 8e6 against 33.0 with the
+    // level-ordered kernel (per launch 1.66 / 1.33 / 4.30 vs 1.55 / 1.31 / 2.79 ms for L1 /
+    // L1^T / U before the acquire-load flags) -- 12 warps per SM (17 KB of shared memory per
+    // warp) do not hide the slice's dependent round trips
     const char *eon = getenv("RSB_BTRSV_NAT");  // read per launch (launches happen at graph capture)
     const bool on = eon && atoi(eon) != 0;
     return on && T.use_nat && T.nat_max_line <= kBnCap;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -1175,6 +1176,9 @@ static int spmv_t_impl(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, i
         }
         return post_launch(ctx);
     }
+    // (An L2 persisting window over 32 / 64 / 79 MB of the gathered vector did not
+    // help A^T y at n = 8e6 -- 1.51 / 1.38 / 1.45 vs 1.39 ms -- and the set-aside
+    // slowed every other kernel: profiles/r02b/kernel_table_spmv_t_persist64.json.)
     if (spmv_tiled()) {
         static const bool occ6 = getenv("RSB_SPMV_T_OCC") && atoi(getenv("RSB_SPMV_T_OCC")) == 6;  // experiments
         if (occ6) {

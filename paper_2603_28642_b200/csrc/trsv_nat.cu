@@ -92,7 +92,7 @@ __device__ __forceinline__ NatSlice nat_slice_load(const NatSrc &s, int n, const
 template <int MODE, int MINB, bool STATIC>
 __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, VecIn a, const double *c, double *x,
                                                           unsigned long long *ticket, int cap, unsigned max_backoff,
-                                                          Gate g) {
+                                                          unsigned min_backoff, Gate g) {
     if (STATIC) {
         if (*(volatile const unsigned long long *)ticket) return;  // the gate's snapshot
     } else if (gated(g)) {
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
                 }
                 if (!__any_sync(full, !done)) break;
                 if (!__any_sync(full, progress)) {
-                    backoff = backoff ? min(backoff * 2, max_backoff) : kNatMinBackoffNs;
+                    backoff = backoff ? min(backoff * 2, max_backoff) : min_backoff;
                     __nanosleep(backoff);
                 } else {
                     backoff = 0;
@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
     }
 }
 
-using NatKernel = void (*)(NatSrc, int, VecIn, const double *, double *, unsigned long long *, int, unsigned, Gate);
+using NatKernel = void (*)(NatSrc, int, VecIn, const double *, double *, unsigned long long *, int, unsigned, unsigned,
+                           Gate);
 
 // MINB resident blocks per SM the registers are budgeted for (4: 64 registers,
 // 6: 40, 8: 32 with spills)
@@ -281,6 +282,8 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
     if (const char *eo = getenv("RSB_NAT_OCC")) occ = std::max(1, std::min(occ, atoi(eo)));  // experiments
     const char *eb = getenv("RSB_NAT_BACKOFF");
     const unsigned max_backoff = eb ? (unsigned)std::max(32, atoi(eb)) : kNatMaxBackoffNs;
+    const char *emb = getenv("RSB_NAT_MINBACKOFF");
+    const unsigned min_backoff = emb ? (unsigned)std::max(8, atoi(emb)) : kNatMinBackoffNs;
     const int64_t nsl = ((int64_t)T.n + 31) / 32;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, (nsl + kNatWarps - 1) / kNatWarps));
     RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
@@ -297,10 +300,10 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, g));
+        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g));
         return RSB_OK;
     }
-    k<<<grid, kNatBlock, smem, ctx->stream>>>(T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, g);
+    k<<<grid, kNatBlock, smem, ctx->stream>>>(T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g);
     return RSB_OK;
 }
 
