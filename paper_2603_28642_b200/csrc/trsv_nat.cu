@@ -143,24 +143,25 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
             const int32_t *gi = s.idx + S0;
             const double *gv = s.val + S0;
             const int span = S1 - S0;
-            for (int i0 = lane; i0 < span; i0 += 128) {
-                int ci[4];
-                double vi[4];
-                unsigned long long pv[4];
+            constexpr int kU = MINB >= 8 ? 2 : 4;  // entries in flight per lane (fewer: fewer registers, more warps)
+            for (int i0 = lane; i0 < span; i0 += 32 * kU) {
+                int ci[kU];
+                double vi[kU];
+                unsigned long long pv[kU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     const bool in = i0 + u * 32 < span;
                     ci[u] = in ? __ldcs(gi + i0 + u * 32) : -1;
                     vi[u] = in ? __ldcs(gv + i0 + u * 32) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     pv[u] = kSentinel;
                     const bool ask = ci[u] >= 0 && (ci[u] < tlo || ci[u] > thi);
                     nat_poll_if(ask, x + (ask ? ci[u] : 0), pv[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kU; ++u) {
                     if (i0 + u * 32 >= span) continue;
                     const bool got = pv[u] != kSentinel;
                     const double xv = __longlong_as_double((long long)pv[u]);
@@ -237,8 +238,19 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
     }
 }
 
+
+
 using NatKernel = void (*)(NatSrc, int, VecIn, const double *, double *, unsigned long long *, int, unsigned, unsigned,
                            Gate);
+
+// (A pipelined static-schedule variant -- a warp owning slices w, w + W, ... and
+// running three stages across them: pointers and right-hand side of s + 2W by
+// plain loads, the span of s + W into a second shared-memory window by 4/8-byte
+// cp.async, polls / chains / publish of s -- measured slower at every warp count:
+// L1 0.92 / 0.54 / 0.42 / 0.36 ms at 8 / 16 / 24 / 32 warps per SM, U 0.69 at best
+// against 0.35 / 0.54 for this kernel (profiles/r02b/trsv_sweep_nat_pipe.json).  With
+// every load prefetched a slice still takes 5-7 us: what a slice waits for is its
+// near dependencies -- 4.7 polling rounds of about a microsecond -- not its loads.)
 
 // MINB resident blocks per SM the registers are budgeted for (4: 64 registers,
 // 6: 40, 8: 32 with spills)
@@ -255,6 +267,7 @@ constexpr int kNatMinBlocks = 6;  // measured at n = 8e6: L1 0.351 / L1^T 0.294 
 constexpr bool kNatStatic = false;
 NatKernel nat_kernel(int mode, int minb, bool st) {
     if (st) return minb <= 4 ? nat_kernel_b<4, true>(mode) : nat_kernel_b<6, true>(mode);
+    if (minb >= 8) return nat_kernel_b<8, false>(mode);
     return minb <= 4 ? nat_kernel_b<4, false>(mode) : nat_kernel_b<6, false>(mode);
 }
 
@@ -267,10 +280,10 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
     const int minb = em ? atoi(em) : kNatMinBlocks;
     const char *es = getenv("RSB_NAT_STATIC");
     const bool st = es ? atoi(es) != 0 : kNatStatic;
-    const int mi = (minb <= 4 ? 0 : 1) + (st ? 2 : 0);
+    const int mi = (minb <= 4 ? 0 : (minb >= 8 && !st ? 4 : 1)) + (st ? 2 : 0);
     NatKernel k = nat_kernel(T.mode, minb, st);
     const size_t smem = trsv_nat_smem(T.mode, T.nat_cap);
-    static size_t granted[4][4] = {};  // grow-only opt-in above 48 KB
+    static size_t granted[4][5] = {};  // grow-only opt-in above 48 KB
     if (smem > 48 * 1024 && smem > granted[T.mode & 3][mi]) {
         RSB_TRY_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         granted[T.mode & 3][mi] = smem;

@@ -143,7 +143,7 @@ def test_wide_levels_use_staged_or_grid(monkeypatch):
 
 @pytest.mark.parametrize("grid", ["levelsync", "levelsync-n4", "lsync", "syncfree", "syncfree-pairs",
                                   "syncfree-unsorted", "syncfree-n4", "static", "static-n4", "natural",
-                                  "natural-cap32", "natural-minb6", "natural-static"])
+                                  "natural-cap32", "natural-minb6", "natural-minb8", "natural-static"])
 @pytest.mark.parametrize("k", [3, 12, 20])
 def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
     """The persistent wide solves (grid schedules): sync-free (the default)
@@ -164,7 +164,7 @@ def test_wide_kernel_every_kind_and_long_tasks(k, grid, monkeypatch):
         monkeypatch.setenv("RSB_TRSV_ORDER", "natural")
     else:
         monkeypatch.setenv("RSB_TRSV_ORDER", "level")
-    if grid == "natural-cap32":  # the smallest window: every slice takes several passes
+    if grid.endswith("cap32"):  # the smallest window: every slice takes several passes
         monkeypatch.setenv("RSB_NAT_CAP", "32")
     if grid.startswith("natural-minb"):
         monkeypatch.setenv("RSB_NAT_MINB", grid[-1])
