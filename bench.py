@@ -516,10 +516,14 @@ def run_b200(args):
     # ---- the batch shard of right-hand sides per GPU
     batch = None
     if Bb is not None and len(Bb) > 1:
-        P.pcgls_batch(S, Bb, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
+        # the shard's right-hand sides in page-locked host memory, as b above
+        Bpin = D.PinnedBuffer(Bb.size)
+        Bp = Bpin.array.reshape(Bb.shape)
+        Bp[:] = Bb
+        P.pcgls_batch(S, Bp, pre, P.CglsConfig(norm_A=norm_a, delta=1e-300, max_iters=max(1, Wm)))
         barrier()
         t0 = time.perf_counter()
-        _, breps = P.pcgls_batch(S, Bb, pre, e2e_cfg)
+        _, breps = P.pcgls_batch(S, Bp, pre, e2e_cfg)
         b_s = barrier_max(time.perf_counter() - t0)
         its = sum(K if r.converged else r.its for r in breps)
         # device-resident: the batched iteration graph replayed K times
@@ -544,7 +548,7 @@ def run_b200(args):
         batch = {"rhs_per_gpu": len(Bb), "value": world * its / b_s, "unit": "RHS-iter/s",
                  "seconds": b_s, "its_each": K, "device": dev,
                  "path": "batched kernels (csrc/bsolver.cu)" if bsv is not None else "one stream per RHS",
-                 "call": f"pcgls_batch(A, B[{len(Bb)} x m] host, pre, CglsConfig(delta=1e-300, "
+                 "call": f"pcgls_batch(A, B[{len(Bb)} x m] pinned host, pre, CglsConfig(delta=1e-300, "
                          f"max_iters={K})), H2D of B and D2H of X inside"}
 
     # ---- time to tolerance: power method + upload + level analysis + solve

@@ -667,44 +667,61 @@ __global__ void __launch_bounds__(kBlk, 2) kb_trsv(TriDev T, VecIn a, const doub
                 for (int q = 0; q < N; ++q)
                     if (f[q] == E) need &= ~(1u << q);
                 if (need == 0 && (!TAIL || len <= N || bt_tail_ready(T, base, N, len, flag, E))) {
+                    // both halves of every row at once, four entries per round: a task
+                    // of <= 4 entries (most of L1's) costs one round trip of gathers
+                    double acc[2][4], dot[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+                    ld4(a.p + ai * kB, acc[0]);
+                    ld4(a.p + ai * kB + 4, acc[1]);
+                    if (c) {
+                        double cv[2][4];
+                        ld4(c + (int64_t)row * kB, cv[0]);
+                        ld4(c + (int64_t)row * kB + 4, cv[1]);
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        double acc[4], dot[4] = {0.0, 0.0, 0.0, 0.0};
-                        ld4(a.p + ai * kB + 4 * h, acc);
-                        if (c) {
-                            double cv[4];
-                            ld4(c + (int64_t)row * kB + 4 * h, cv);
+                        for (int h = 0; h < 2; ++h)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) acc[q] = __dadd_rn(acc[q], cv[q]);
-                        }
-                        double xv[N][4];
+                            for (int q = 0; q < 4; ++q) acc[h][q] = __dadd_rn(acc[h][q], cv[h][q]);
+                    }
 #pragma unroll
-                        for (int e = 0; e < N; ++e) {
-                            if (cols[e] >= 0)
-                                ld4(x + (int64_t)cols[e] * kB + 4 * h, xv[e]);
-                            else
-                                xv[e][0] = xv[e][1] = xv[e][2] = xv[e][3] = 0.0;
-                        }
+                    for (int e0 = 0; e0 < N; e0 += 4) {
+                        if (e0 > 0 && e0 >= len) break;
+                        double xv[4][2][4];
 #pragma unroll
-                        for (int e = 0; e < N; ++e) {
-                            if (e >= len) break;
+                        for (int u = 0; u < 4; ++u) {
+                            if (cols[e0 + u] >= 0) {
+                                ld4(x + (int64_t)cols[e0 + u] * kB, xv[u][0]);
+                                ld4(x + (int64_t)cols[e0 + u] * kB + 4, xv[u][1]);
+                            } else {
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                if (!(MODE & 1)) {
-                                    if (xv[e][q] != 0.0) acc[q] = __dsub_rn(acc[q], __dmul_rn(vals[e], xv[e][q]));
-                                } else {
-                                    dot[q] = fma(vals[e], xv[e][q], dot[q]);
-                                }
+                                for (int h = 0; h < 2; ++h) xv[u][h][0] = xv[u][h][1] = xv[u][h][2] = xv[u][h][3] = 0.0;
                             }
                         }
-                        if (TAIL && len > N) bt_tail<MODE>(T, base, N, len, h, x, acc, dot);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (e0 + u >= len) break;
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    if (!(MODE & 1)) {
+                                        if (xv[u][h][q] != 0.0)
+                                            acc[h][q] = __dsub_rn(acc[h][q], __dmul_rn(vals[e0 + u], xv[u][h][q]));
+                                    } else {
+                                        dot[h][q] = fma(vals[e0 + u], xv[u][h][q], dot[h][q]);
+                                    }
+                                }
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (TAIL && len > N) bt_tail<MODE>(T, base, N, len, h, x, acc[h], dot[h]);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            if ((MODE & 1) && len > 0) acc[q] = __dsub_rn(acc[q], dot[q]);
-                            if (MODE & 2) acc[q] = __ddiv_rn(acc[q], d);
+                            if ((MODE & 1) && len > 0) acc[h][q] = __dsub_rn(acc[h][q], dot[h][q]);
+                            if (MODE & 2) acc[h][q] = __ddiv_rn(acc[h][q], d);
                         }
-                        st4(x + (int64_t)row * kB + 4 * h, acc);
                     }
+                    st4(x + (int64_t)row * kB, acc[0]);
+                    st4(x + (int64_t)row * kB + 4, acc[1]);
                     st_flag_release(flag + row, E);
                     done = true;
                 }
