@@ -248,9 +248,9 @@ __global__ void __launch_bounds__(kBlk) kb_spmv_rows(Compressed A, VecIn x, doub
 }
 
 // (CSC products with an octet of lanes per column straight from global
-// memory, the CSR kernel's scheme, measured far slower than the tiled kernel:
-// 87 vs 36.5 ms per batched iteration at n = 8e6 -- a column's pairwise order
-// needs its products 8 at a time, two dependent round trips per column.)
+// memory, the CSR kernel's scheme, measured slower than the tiled kernel twice:
+// through bline_pw 87 vs 36.5 ms per batched iteration at n = 8e6, and with a
+// register version for columns of <= 16 entries (L2^T w only) 37.4 vs 32.6.)
 
 // ---- a @ b per RHS in the context's OpenBLAS order.  Block = 256 threads:
 // thread t runs accumulator chain t >> 3 (of the 32 the OpenBLAS kernel
