@@ -295,6 +295,10 @@ int rsb_cholesky_factorize(int64_t s, double *g);
 int rsb_column_scale(int64_t ncols, const int64_t *col_ptr, const double *values,
                      double *scaled_values, double *norms);
 
+/* the same on the device (upload, one kernel, download): bit-identical */
+int rsb_column_scale_device(rsb_ctx *ctx, int64_t ncols, const int64_t *col_ptr, const double *values,
+                            double *scaled_values, double *norms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -108,6 +108,7 @@ _SIGS = {
     "rsb_build_y_explicit": [i64, i64, vp, vp, vp, vp, vp, vp, i64p, vp, vp, vp],
     "rsb_cholesky_factorize": [i64, vp],
     "rsb_column_scale": [i64, vp, vp, vp, vp],
+    "rsb_column_scale_device": [vp, i64, vp, vp, vp, vp],
     "rsb_dense_build": [vp, vp, ctypes.c_int, ctypes.POINTER(vp)],
     "rsb_dense_build_sizes": [vp, i64p, i64p, i64p, f64p],
     "rsb_dense_build_copy": [vp, vp, vp, vp, vp, vp],

@@ -25,6 +25,7 @@
 #include <cub/device/device_scan.cuh>
 #include <vector>
 
+#include "device_common.cuh"
 #include "rsb_internal.h"
 
 struct rsb_dbuild {
@@ -577,6 +578,35 @@ void dbuild_free(rsb_dbuild *B) {
 }
 
 }  // namespace
+
+// column_scale (sc.py:405-425) on the device: sq_j = reduceat(v * v) = p0 +
+// pairwise(p1 ..) per column (numpy's order), norms = sqrt(sq), values /
+// norms[column] -- IEEE multiply, add, sqrt and divide, so bit-identical to
+// the reference and to the host version (rsb_column_scale).
+namespace {
+struct SqTerm {
+    const double *v;
+    __device__ double operator()(int64_t k) const { return __dmul_rn(v[k], v[k]); }
+};
+__global__ void k_colscale(int64_t ncols, const int64_t *ptr, const double *val, double *scaled, double *norms,
+                           int *empty_min) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < ncols; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = ptr[j], hi = ptr[j + 1];
+        if (hi <= lo) {
+            atomicMin(empty_min, (int)j);
+            norms[j] = 0.0;
+            continue;
+        }
+        const SqTerm t{val + lo};
+        const int64_t m = hi - lo - 1;
+        const double s2 = __dadd_rn(t(0), m <= 128 ? pw_leaf(t, 1, m) : Pairwise<25, SqTerm>::sum(t, 1, m));
+        const double nj = __dsqrt_rn(s2);
+        norms[j] = nj;
+        for (int64_t k = lo; k < hi; ++k) scaled[k] = __ddiv_rn(val[k], nj);
+    }
+}
+}  // namespace
+
 }  // namespace rsb
 
 using namespace rsb;
@@ -710,6 +740,69 @@ int rsb_cholesky_factorize_device(rsb_ctx *ctx, int64_t s, double *g, int where)
     cudaStreamSynchronize(ctx->stream);
     dev_free(ctx, d, std::max<size_t>(1, ss) * sizeof(double));
     return rc;
+}
+
+
+int rsb_column_scale_device(rsb_ctx *ctx, int64_t ncols, const int64_t *col_ptr, const double *values,
+                            double *scaled_values, double *norms) {
+    RSB_TRY_CUDA(cudaSetDevice(ctx->device));
+    if (ncols < 0) {
+        set_error("negative size");
+        return RSB_EINVAL;
+    }
+    if (ncols == 0) return RSB_OK;
+    if (ncols > INT32_MAX) {
+        set_error("too many columns");
+        return RSB_EINVAL;
+    }
+    const int64_t nnz = col_ptr[ncols];
+    int64_t *d_ptr = nullptr;
+    double *d_val = nullptr, *d_out = nullptr, *d_norm = nullptr;
+    int *d_empty = nullptr;
+    int rc = RSB_OK;
+    auto free_all = [&]() {
+        cudaStreamSynchronize(ctx->stream);
+        if (d_ptr) dev_free(ctx, d_ptr, (ncols + 1) * sizeof(int64_t));
+        if (d_val) dev_free(ctx, d_val, std::max<int64_t>(1, nnz) * sizeof(double));
+        if (d_out) dev_free(ctx, d_out, std::max<int64_t>(1, nnz) * sizeof(double));
+        if (d_norm) dev_free(ctx, d_norm, ncols * sizeof(double));
+        if (d_empty) dev_free(ctx, d_empty, sizeof(int));
+    };
+    if ((rc = dev_alloc(ctx, (void **)&d_ptr, (ncols + 1) * sizeof(int64_t))) != RSB_OK ||
+        (rc = dev_alloc(ctx, (void **)&d_val, std::max<int64_t>(1, nnz) * sizeof(double))) != RSB_OK ||
+        (rc = dev_alloc(ctx, (void **)&d_out, std::max<int64_t>(1, nnz) * sizeof(double))) != RSB_OK ||
+        (rc = dev_alloc(ctx, (void **)&d_norm, ncols * sizeof(double))) != RSB_OK ||
+        (rc = dev_alloc(ctx, (void **)&d_empty, sizeof(int))) != RSB_OK) {
+        free_all();
+        return rc;
+    }
+    const int big = INT32_MAX;
+    int h_empty = big;
+    cudaError_t e = cudaMemcpyAsync(d_ptr, col_ptr, (ncols + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpyAsync(d_val, values, nnz * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_empty, &big, sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) {
+        k_colscale<<<blocks_for(ncols), kT, 0, ctx->stream>>>(ncols, d_ptr, d_val, d_out, d_norm, d_empty);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_empty, d_empty, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess && h_empty != big) {
+        set_error("cannot scale zero column %d", h_empty);
+        free_all();
+        return RSB_EINVAL;
+    }
+    if (e == cudaSuccess && nnz)
+        e = cudaMemcpyAsync(scaled_values, d_out, nnz * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(norms, d_norm, ncols * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    free_all();
+    if (e != cudaSuccess) {
+        set_error("device column_scale failed: %s", cudaGetErrorString(e));
+        return RSB_ECUDA;
+    }
+    return RSB_OK;
 }
 
 }  // extern "C"

@@ -104,8 +104,14 @@ def power_method_norm2(A, iters=100, seed=0) -> float:
     return float(est[0])
 
 
-def column_scale(A):
-    """Scale every column of A to unit 2-norm (sc.py:405-425), host native."""
+def column_scale(A, *, setup: str | None = None):
+    """Scale every column of A to unit 2-norm (sc.py:405-425), bit-identical.
+    setup='host' (default; env RSB_SETUP) runs the native host loop,
+    'device' one kernel (csrc/dbuild.cu k_colscale: the same per-column
+    p0 + pairwise order, IEEE sqrt and divide)."""
+    where = setup if setup is not None else os.environ.get("RSB_SETUP", "host")
+    if where not in ("host", "device"):
+        raise ValueError("setup must be 'host' or 'device'")
     cp = L.i64c(A.col_ptr)
     counts = np.diff(cp)
     empty = np.flatnonzero(counts == 0)
@@ -114,7 +120,11 @@ def column_scale(A):
     vals = L.f64c(A.values)
     scaled = np.empty_like(vals)
     norms = np.empty(int(A.ncols))
-    L.check(L.lib().rsb_column_scale(int(A.ncols), L.ptr(cp), L.ptr(vals), L.ptr(scaled), L.ptr(norms)))
+    if where == "device":
+        L.check(L.lib().rsb_column_scale_device(get_context().h, int(A.ncols), L.ptr(cp), L.ptr(vals), L.ptr(scaled),
+                                                L.ptr(norms)))
+    else:
+        L.check(L.lib().rsb_column_scale(int(A.ncols), L.ptr(cp), L.ptr(vals), L.ptr(scaled), L.ptr(norms)))
     out = CscMatrix(A.nrows, A.ncols, cp.copy(), L.i64c(A.row_idx).copy(), scaled)
     return out, ColumnScaling(norms)
 

@@ -117,3 +117,29 @@ def test_device_build_empty_l2_and_bad_setup():
     Y, S, F, _ = dense_build_device(f0, what=2)
     assert (Y.nrows, Y.ncols, Y.nnz) == (0, n, 0)
     assert S.a.shape == (0, 0) and F.a.shape == (0, 0)
+
+
+def test_column_scale_device_bitwise():
+    """column_scale (sc.py:405-425) on the device against the native host
+    version (itself pinned to the reference): short columns, columns longer
+    than numpy's pairwise leaf (128) and than its 8-term block, an empty
+    column's error."""
+    import paper_2603_28642_b200 as P
+    from paper_2603_28642_b200 import workloads as W
+
+    rng = np.random.default_rng(5)
+    mats = [W.config4(seed=4, n=20_000, nrhs=0)[0], W.config2(seed=2, n=3000)[0]]
+    # one matrix with columns of 1 .. 400 entries
+    rows, cols = [], []
+    for j, k in enumerate([1, 2, 7, 8, 9, 15, 16, 17, 127, 128, 129, 130, 257, 400]):
+        rows += sorted(rng.choice(500, size=k, replace=False).tolist())
+        cols += [j] * k
+    mats.append(P.CscMatrix.from_coo(500, 14, np.array(rows), np.array(cols), rng.standard_normal(len(rows))))
+    for A in mats:
+        Sh, ch = P.column_scale(A, setup="host")
+        Sd, cd = P.column_scale(A, setup="device")
+        assert np.array_equal(Sh.values, Sd.values) and np.array_equal(ch.scale, cd.scale)
+        assert np.array_equal(Sh.col_ptr, Sd.col_ptr) and np.array_equal(Sh.row_idx, Sd.row_idx)
+    E = P.CscMatrix.from_coo(4, 3, np.array([0, 1]), np.array([0, 2]), np.array([1.0, 2.0]))
+    with pytest.raises(ValueError, match="zero column 1"):
+        P.column_scale(E, setup="device")
