@@ -53,6 +53,19 @@ def test_reference_multithread_dots(threads):
             assert _device_dot(a, b) == want, (t, n)
 
 
+def test_b200_host_multithread_dots(threads):
+    """The device's T-thread dot order against numpy run on the B200 box's own
+    16-core host at T = 12 and 16 (tests/golden/dots_mt_host.json), incl. the
+    config-4 lengths 8e6 and 1.6e7."""
+    g = golden_json("dots_mt_host.json")
+    for t in ("12", "16"):
+        threads(int(t))
+        rng = np.random.default_rng(g["seed"])
+        for n, want in zip(g["lens"], g["dots"][t]):
+            a, b = rng.standard_normal(n), rng.standard_normal(n)
+            assert _device_dot(a, b) == want, (t, n)
+
+
 @pytest.mark.parametrize("t", [2, 3, 7, 16, 33, 64])
 @pytest.mark.parametrize("n", [10000, 10001, 98304, 24577 * 7, 1_000_003, 1_500_000, 4_000_001])
 def test_device_dot_threads_vs_oracle(threads, t, n):

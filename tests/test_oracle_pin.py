@@ -126,6 +126,20 @@ def test_oracle_blas_threads_dot_order(blas_threads):
             assert O.dot(a, b) == want, (t, n)
 
 
+def test_oracle_blas_threads_dot_order_b200_host(blas_threads):
+    """numpy on the B200 box's 16-core host at OPENBLAS_NUM_THREADS = 1 .. 16
+    (dots_mt_host.json, written there by scripts/dot_probe_host.py
+    --write-golden), up to the config-4 dot lengths 8e6 and 1.6e7."""
+    g = golden_json("dots_mt_host.json")
+    assert g["cores"] >= 16 and "16" in g["dots"]
+    for t in ("12", "16"):
+        blas_threads(int(t))
+        rng = np.random.default_rng(g["seed"])
+        for n, want in zip(g["lens"], g["dots"][t]):
+            a, b = rng.standard_normal(n), rng.standard_normal(n)
+            assert O.dot(a, b) == want, (t, n)
+
+
 def test_oracle_pcgls_blas_threads_golden(blas_threads):
     """The whole reference pipeline run with OPENBLAS_NUM_THREADS=8 on a
     112^2-grid config 1 (every n- and m-long dot and norm threaded)."""
