@@ -275,10 +275,13 @@ def ncu_traffic(workload_key, cls):
         with open(path) as fh:
             d = json.load(fh).get(workload_key)
         if d and cls in d:
-            return d[cls].get("dram_bytes_per_iteration"), d[cls].get("source")
+            per = d[cls].get("per_solve") or d[cls].get("per_product") or {}
+            detail = {k: {"dram_bytes": v.get("dram_bytes"), "ncu_ms": v.get("ncu_ms"),
+                          "l1tex_pct": v.get("l1tex_pct"), "l2_hit_pct": v.get("l2_hit_pct")} for k, v in per.items()}
+            return d[cls].get("dram_bytes_per_iteration"), d[cls].get("source"), detail
     except (OSError, ValueError):
         pass
-    return None, "no ncu capture committed for this workload"
+    return None, "no ncu capture committed for this workload", {}
 
 
 def spmv_bytes(nnz, rows, cols):
@@ -589,11 +592,12 @@ def run_b200(args):
     for cls, label, by, cnt, ms in (
             ("solves", "sparse triangular solves", tbytes, counts, float(tri_ms[0])),
             ("products", "sparse products (A x, A^T y, L2 t, L2^T w)", pbytes, pcounts, float(prod_ms[0]))):
-        tr, tr_src = ncu_traffic(wkey, cls)
+        tr, tr_src, tr_detail = ncu_traffic(wkey, cls)
         ach = (by * K) / (ms / 1e3) / 1e9 if ms > 0 else 0.0
         classes[cls] = {"kernel": f"{label}, {sum(cnt.values())} per iteration ({cnt})", "bound": "hbm",
                         "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "peak_kind": peak_kind,
-                        "traffic": tr, "traffic_source": tr_src, "algorithmic_bytes_per_iteration": by,
+                        "traffic": tr, "traffic_source": tr_src, "ncu_per_kernel": tr_detail,
+                        "algorithmic_bytes_per_iteration": by,
                         "ms_per_iteration": ms / K, "share_of_step": ms / float(it_ms[0])}
     dom = max(classes, key=lambda c: classes[c]["ms_per_iteration"])
     roofline = dict(classes[dom])

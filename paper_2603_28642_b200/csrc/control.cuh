@@ -80,8 +80,13 @@ struct ApplyWs {
     double *u = nullptr, *w = nullptr;                                  // s
     double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;            // s
     double *cg_a = nullptr, *cg_b = nullptr, *cg_c = nullptr;            // n
+    double *cg_b2 = nullptr;  // n: cg_b of the odd inner-CG steps (a solve fills its successor's output, TrsvChain)
     CgState *cg = nullptr;
     TriWs tri;
+    // A solver's own workspace (only enqueue_apply touches it): t1, the first
+    // solve's output, holds the sentinel between applications -- filled once
+    // at allocation, then by every application's last solve.
+    bool carry = false;
 };
 
 }  // namespace rsb

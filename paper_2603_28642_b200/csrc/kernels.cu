@@ -529,7 +529,7 @@ __device__ __forceinline__ double canonical(double v) {
 // chain waits on shared-memory, not global-memory, latency.
 __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const double *a_all, const double *b_all,
                                                          double *out, int sqrt_out, Gate g, const int *need,
-                                                         DotChunks ch) {
+                                                         DotChunks ch, int norm_stages) {
     if (need && !*(volatile const int *)need) return;
     if (__shfl_sync(0xffffffffu, gated(g) ? 1 : 0, 0)) {  // still count this chunk (dot_combine)
         if (threadIdx.x == 0) dot_combine(0.0, out, sqrt_out, ch, true);
@@ -548,10 +548,17 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
     // buffer) to the even element above its end, except past the end of the
     // vectors, where the last odd element is loaded by lane 0 instead
     const int shift = (int)(lo & 1);
+    // a norm (a.a): one operand stream -- a chunk is bounded by its SM's
+    // ingest rate (~16 B/cycle against the 64 the chain could use), so half
+    // the bytes is close to half the time; same products, same order
+    // and its buffers hold twice the stages
+    const bool same = a_all == b_all;
+    const int nst = same ? norm_stages : kDotStages;
+    const size_t sbuf = same ? kBuf : 2 * kBuf;  // doubles per stage
     const int64_t n32 = (n & ~(int64_t)15) & ~(int64_t)31;
     const int64_t nch = (n32 + kDotChunk - 1) / kDotChunk;
     if (lane == 0) {
-        for (int st = 0; st < kDotStages; ++st) mbar_init(&bar[st], 1);
+        for (int st = 0; st < nst; ++st) mbar_init(&bar[st], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -563,25 +570,25 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
         if (patch) c1 -= 2;
     };
     auto issue = [&](int64_t c) {
-        const int st = (int)(c % kDotStages);
+        const int st = (int)(c % nst);
         int64_t c0, c1;
         bool patch;
         span(c, c0, c1, patch);
         const unsigned bytes = (unsigned)((c1 - c0) * 8);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bar[st], 2 * bytes);
+        mbar_expect_tx(&bar[st], same ? bytes : 2 * bytes);
         if (bytes) {
-            bulk_g2s(dbuf + (size_t)st * 2 * kBuf, a_all + c0, bytes, &bar[st]);
-            bulk_g2s(dbuf + (size_t)st * 2 * kBuf + kBuf, b_all + c0, bytes, &bar[st]);
+            bulk_g2s(dbuf + (size_t)st * sbuf, a_all + c0, bytes, &bar[st]);
+            if (!same) bulk_g2s(dbuf + (size_t)st * sbuf + kBuf, b_all + c0, bytes, &bar[st]);
         }
     };
     if (lane == 0)
-        for (int64_t c = 0; c < min((int64_t)kDotStages, nch); ++c) issue(c);
+        for (int64_t c = 0; c < min((int64_t)nst, nch); ++c) issue(c);
     double acc = 0.0;
     for (int64_t c = 0; c < nch; ++c) {
-        const int st = (int)(c % kDotStages);
-        mbar_wait_spin(&bar[st], (unsigned)((c / kDotStages) & 1));
-        double *buf_a = dbuf + (size_t)st * 2 * kBuf, *buf_b = buf_a + kBuf;
+        const int st = (int)(c % nst);
+        mbar_wait_spin(&bar[st], (unsigned)((c / nst) & 1));
+        double *buf_a = dbuf + (size_t)st * sbuf, *buf_b = same ? buf_a : buf_a + kBuf;
         {
             int64_t c0, c1;
             bool patch;
@@ -625,7 +632,7 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
         }
         for (int k = full_groups * G; k < steps; ++k) acc = fma(sa[32 * k], sb[32 * k], acc);
         __syncwarp();
-        if (lane == 0 && c + kDotStages < nch) issue(c + kDotStages);
+        if (lane == 0 && c + nst < nch) issue(c + nst);
     }
     const double d = warp_blas_finish(acc, n, [&](int64_t i) { return a[i]; }, [&](int64_t i) { return b[i]; });
     if (lane == 0) dot_combine(d, out, sqrt_out, ch, false);
@@ -1228,8 +1235,13 @@ int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int ep
 }
 
 int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g,
-                const TriWs *ws) {
+                const TriWs *ws, TrsvChain chain) {
     if (T.n == 0) return RSB_OK;
+    const bool nat = trsv_wants_prefill(T);
+    if (chain.fill_next && !nat) {  // no in-kernel fill in this variant
+        RSB_TRY(launch_fill(ctx, chain.fill_next, T.n, kSentinel, Gate{}));
+        chain.fill_next = nullptr;
+    }
     const bool trace = ctx->tracing && ctx->trace_n + 2 <= 64;
     if (trace)
         RSB_TRY_CUDA(cudaEventRecordWithFlags(ctx->trace_ev[ctx->trace_n++], ctx->stream, cudaEventRecordExternal));
@@ -1276,7 +1288,8 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
         RSB_TRY(launch_trsv_lsync(ctx, T, v, ws ? ws->ls_cnt : T.ls_cnt, a, c, x, g));
     } else if (T.wide && T.use_nat) {
         RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
-        RSB_TRY(launch_trsv_nat(ctx, T, v, a, c, x, g));  // sentinel fill, then the solve (counted below)
+        // sentinel fill unless the chain's previous solve did it, then the solve (counted below)
+        RSB_TRY(launch_trsv_nat(ctx, T, v, a, c, x, g, chain.prefilled, chain.fill_next));
     } else if (T.wide && T.level_sync) {
         // level-synchronous cooperative solve (trsv_ls.cu), the default for wide DAGs
         RSB_TRY(launch_trsv_ls(ctx, T, v, a, c, x, reinterpret_cast<unsigned *>(v.ticket), g, 1, nullptr, 0));
@@ -1375,8 +1388,12 @@ int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_
     const int64_t per_chunk = n / ch.T;
     const bool plain = !a.g && !b.g && !a.off && !b.off && ((uintptr_t)a.p % 16 == 0) && ((uintptr_t)b.p % 16 == 0);
     if (plain && per_chunk >= 2 * kDotChunk) {
-        const size_t smem = (size_t)kDotStages * 2 * (kDotChunk + 2) * 8 + kDotStages * 8;
-        k_dot_exact_staged<<<ch.T, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need, ch);
+        const size_t smem = (size_t)kDotStages * 2 * (kDotChunk + 2) * 8 + 2 * kDotStages * 8;
+        static const int norm_stages = [] {  // experiments: stages of the one-stream norm (2 .. 2 * kDotStages)
+            const char *e = getenv("RSB_DOT_NORM_STAGES");
+            return e ? std::max(2, std::min(2 * kDotStages, atoi(e))) : 2 * kDotStages;
+        }();
+        k_dot_exact_staged<<<ch.T, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need, ch, norm_stages);
         return post_launch(ctx);
     }
     k_dot_exact<<<ch.T, 32, 0, ctx->stream>>>(n, a, b, out, sqrt_out, g, need, ch);
@@ -1384,7 +1401,7 @@ int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_
 }
 
 int prepare_kernels() {
-    const int smem = kDotStages * 2 * (kDotChunk + 2) * 8 + kDotStages * 8;
+    const int smem = kDotStages * 2 * (kDotChunk + 2) * 8 + 2 * kDotStages * 8;
     RSB_TRY_CUDA(cudaFuncSetAttribute(k_dot_exact_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return RSB_OK;
 }

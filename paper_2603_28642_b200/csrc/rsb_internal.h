@@ -415,7 +415,11 @@ int launch_trsv_wide(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, 
 // wide schedule uses it (RSB_TRSV_ORDER=natural | level overrides)
 constexpr int64_t kNatNear = 1 << 18;
 constexpr int kNatMaxCap = 1024;
-int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g);
+// prefilled: x already holds the sentinel (the previous solve of the chain
+// wrote it); fill_next: an n-vector this launch also fills with the sentinel
+// (the next solve's output), gate or no gate
+int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g,
+                    bool prefilled = false, double *fill_next = nullptr);
 size_t trsv_nat_smem(int mode, int cap);
 int tri_setup_nat(rsb_mat *T, int kind, TriSched *S);
 TaskSrc tri_task_src(const rsb_mat *T, int kind);
@@ -470,8 +474,21 @@ int launch_spmv(rsb_ctx *ctx, const Compressed &A, VecIn x, double *y, int epi, 
 int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int epi, VecIn e, Gate g);
 // triangular solve of a schedule: x(row) = solve with rhs(row) = a(row) [+ c[row]]
 // (ws: the launcher's scratch; nullptr uses the schedule's own, for standalone calls)
+// A chain of solves whose outputs must hold the sentinel before they start
+// (the sync-free kernels): a solve fills its successor's output while it runs
+// -- the solves are latency-bound, the stores ride along -- instead of one
+// fill launch per solve.  On return fill_next holds the sentinel whatever the
+// gate says (by the solve kernel, or by a fill launch where the variant has
+// no in-kernel fill).
+struct TrsvChain {
+    bool prefilled = false;       // x already holds the sentinel
+    double *fill_next = nullptr;  // n-vector to fill with the sentinel (nullptr: none)
+};
+inline bool trsv_wants_prefill(const TriSched &T) { 
+    return T.n > 0 && !T.single_cta && !T.level_launch && !T.lsync && T.wide && T.use_nat;  // launch_trsv's dispatch
+}
 int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, double *x, Gate g,
-                const TriWs *ws = nullptr);
+                const TriWs *ws = nullptr, TrsvChain chain = TrsvChain{});
 // out[0] = a.b (sqrt_out: sqrt(a.b)) in the context's dot order; need: optional
 // flag that must be nonzero for the dot to run
 int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_out, Gate g,

@@ -194,12 +194,13 @@ using namespace rsb;
 // ---------------------------------------------------------------------------
 namespace {
 
-int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W) {
+int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W, bool carry = false) {
     W.ctx = ctx;
     W.n = P->n;
     W.s = P->s;
     const size_t n8 = P->n * sizeof(double), s8 = P->s * sizeof(double);
-    for (double **q : {&W.t1, &W.t2, &W.t3, &W.v, &W.cg_a, &W.cg_b, &W.cg_c}) RSB_TRY(dev_alloc(ctx, (void **)q, n8));
+    for (double **q : {&W.t1, &W.t2, &W.t3, &W.v, &W.cg_a, &W.cg_b, &W.cg_c, &W.cg_b2})
+        RSB_TRY(dev_alloc(ctx, (void **)q, n8));
     for (double **q : {&W.u, &W.w, &W.cg_r, &W.cg_p, &W.cg_q}) RSB_TRY(dev_alloc(ctx, (void **)q, s8));
     RSB_TRY(dev_alloc(ctx, (void **)&W.cg, sizeof(CgState)));
     RSB_TRY_CUDA(cudaMemsetAsync(W.cg, 0, sizeof(CgState), ctx->stream));
@@ -207,31 +208,64 @@ int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W) {
     for (const TriSched *T : {P->tL1, P->tL1T, P->tU})
         if (T) cap = std::max(cap, T->padded_n);
     RSB_TRY(tri_ws_alloc(ctx, W.tri, cap));
+    // the implicit-Y application starts with L1: r1 -> t1 and never reads t1
+    // after its first product, so its last solve can refill it
+    W.carry = carry && P->s > 0 && P->y_mode != RSB_Y_EXPLICIT && trsv_wants_prefill(*P->tL1);
+    if (W.carry) RSB_TRY(launch_fill(ctx, W.t1, P->n, kSentinel, Gate{}));
     return RSB_OK;
 }
 
 void ws_free(ApplyWs &W) {
     if (!W.ctx) return;
     const size_t n8 = W.n * sizeof(double), s8 = W.s * sizeof(double);
-    for (double *q : {W.t1, W.t2, W.t3, W.v, W.cg_a, W.cg_b, W.cg_c}) dev_free(W.ctx, q, n8);
+    for (double *q : {W.t1, W.t2, W.t3, W.v, W.cg_a, W.cg_b, W.cg_c, W.cg_b2}) dev_free(W.ctx, q, n8);
     for (double *q : {W.u, W.w, W.cg_r, W.cg_p, W.cg_q}) dev_free(W.ctx, q, s8);
     dev_free(W.ctx, W.cg, sizeof(CgState));
     tri_ws_free(W.ctx, W.tri);
     W.ctx = nullptr;
 }
 
+// The solves of one application form a chain: each fills the next one's output
+// with the sentinel where that solve wants it (TrsvChain).  `ready` is the
+// vector the previous solve filled.
+struct SolveChain {
+    rsb_ctx *ctx;
+    ApplyWs &W;
+    Gate g;
+    double *ready;
+    int run(const TriSched &T, VecIn a, const double *c, double *x, const TriSched *next, double *next_x) {
+        TrsvChain ch;
+        ch.prefilled = ready != nullptr && ready == x;
+        ch.fill_next = (next && next_x && trsv_wants_prefill(*next)) ? next_x : nullptr;
+        RSB_TRY(launch_trsv(ctx, T, a, c, x, g, &W.tri, ch));
+        ready = ch.fill_next;
+        return RSB_OK;
+    }
+};
+
 // q = S p = p + L2 L1^{-1} L1^{-T} L2^T p  (s_matvec_implicit, pc.py:149-154)
-int enqueue_s_matvec(rsb_pre *P, ApplyWs &W, const double *p, double *q, Gate g) {
+// cb: the vector between the two solves; after: the solve that follows this
+// product in the chain and its output (nullptr: none)
+int enqueue_s_matvec(rsb_pre *P, ApplyWs &W, const double *p, double *q, Gate g, SolveChain *chain = nullptr,
+                     double *cb = nullptr, const TriSched *after = nullptr, double *after_x = nullptr) {
     rsb_ctx *ctx = W.ctx;
+    SolveChain local{ctx, W, g, nullptr};
+    SolveChain &C = chain ? *chain : local;
+    if (!cb) cb = W.cg_b;
+    const Gate outer = C.g;
+    C.g = g;
     RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{p, nullptr, 0}, W.cg_a, EPI_STORE, VecIn{}, g));
-    RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{W.cg_a, nullptr, 0}, nullptr, W.cg_b, g, &W.tri));
-    RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{W.cg_b, nullptr, 0}, nullptr, W.cg_c, g, &W.tri));
+    RSB_TRY(C.run(*P->tL1T, VecIn{W.cg_a, nullptr, 0}, nullptr, cb, P->tL1, W.cg_c));
+    RSB_TRY(C.run(*P->tL1, VecIn{cb, nullptr, 0}, nullptr, W.cg_c, after, after_x));
+    C.g = outer;
     RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{W.cg_c, nullptr, 0}, q, EPI_ADD, VecIn{p, nullptr, 0}, g));
     return RSB_OK;
 }
 
 // w = _cg_fixed_steps(S, u, k)  (pc.py:284-310), result in W.w
-int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
+// after / after_x: the solve that follows the inner CG in the chain
+int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer, SolveChain &C, const TriSched *after,
+               double *after_x) {
     rsb_ctx *ctx = W.ctx;
     const int64_t s = P->s;
     CgState *cg = W.cg;
@@ -241,8 +275,11 @@ int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
     k_cg_start<<<1, 1, 0, ctx->stream>>>(cg, outer);
     RSB_TRY(chk(ctx));
     Gate g{outer.a, &cg->stop};
+    auto cb_of = [&](int it) { return (it & 1) ? W.cg_b2 : W.cg_b; };
     for (int it = 0; it < P->cg_iters; ++it) {
-        RSB_TRY(enqueue_s_matvec(P, W, W.cg_p, W.cg_q, g));
+        const bool last = it + 1 == P->cg_iters;
+        RSB_TRY(enqueue_s_matvec(P, W, W.cg_p, W.cg_q, g, &C, cb_of(it), last ? after : P->tL1T,
+                                 last ? after_x : cb_of(it + 1)));
         RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_p, nullptr, 0}, VecIn{W.cg_q, nullptr, 0}, &cg->pq, 0, g, nullptr));
         k_cg_alpha<<<1, 1, 0, ctx->stream>>>(cg, g);
         RSB_TRY(chk(ctx));
@@ -251,7 +288,7 @@ int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
         // here and the next application starts from k_cg_init / k_cg_start
         // (which resets the stop flag), so they are not enqueued -- w, and so
         // every apply, is unchanged bit for bit
-        if (it + 1 == P->cg_iters) break;
+        if (last) break;
         RSB_TRY(launch_axpy(ctx, W.cg_r, W.cg_q, &cg->alpha, -1, s, g));
         RSB_TRY(launch_dot(ctx, s, VecIn{W.cg_r, nullptr, 0}, VecIn{W.cg_r, nullptr, 0}, &cg->rho_new, 0, g, nullptr));
         k_cg_beta<<<1, 1, 0, ctx->stream>>>(cg, g);
@@ -264,12 +301,18 @@ int enqueue_cg(rsb_pre *P, ApplyWs &W, const double *u, Gate outer) {
 // h = apply(r1, r2)  (pc.py:175-186)
 int enqueue_apply(rsb_pre *P, ApplyWs &W, VecIn r1, VecIn r2, double *h, Gate g) {
     rsb_ctx *ctx = W.ctx;
+    SolveChain C{ctx, W, g, W.carry ? W.t1 : nullptr};
     if (P->s > 0) {
+        const bool expl = P->y_mode == RSB_Y_EXPLICIT;
+        // the first solve after w = solve_S(u), and its output
+        const TriSched *back = expl ? P->tL1 : P->tL1T;
+        double *back_x = expl ? W.v : W.t3;
+        const bool cg = P->s_mode != RSB_S_DENSE && P->s_mode != RSB_S_IDENTITY;
         // u = r2 - Y r1
-        if (P->y_mode == RSB_Y_EXPLICIT) {
+        if (expl) {
             RSB_TRY(launch_spmv(ctx, P->Y->csr(), r1, W.u, EPI_SUB_FROM, r2, g));
         } else {
-            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, W.t1, g, &W.tri));
+            RSB_TRY(C.run(*P->tL1, r1, nullptr, W.t1, cg ? P->tL1T : back, cg ? W.cg_b : back_x));
             RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{W.t1, nullptr, 0}, W.u, EPI_SUB_FROM, r2, g));
         }
         // w = solve_S(u)
@@ -279,21 +322,22 @@ int enqueue_apply(rsb_pre *P, ApplyWs &W, VecIn r1, VecIn r2, double *h, Gate g)
         } else if (P->s_mode == RSB_S_IDENTITY) {
             w = W.u;
         } else {
-            RSB_TRY(enqueue_cg(P, W, W.u, g));
+            RSB_TRY(enqueue_cg(P, W, W.u, g, C, back, back_x));
         }
         // y = r1 + Y^T w ; v = L1^{-1} y
-        if (P->y_mode == RSB_Y_EXPLICIT) {
+        if (expl) {
             RSB_TRY(launch_spmv_t(ctx, P->Y->csc(), VecIn{w, nullptr, 0}, W.t3, EPI_ADD, r1, g));
-            RSB_TRY(launch_trsv(ctx, *P->tL1, VecIn{W.t3, nullptr, 0}, nullptr, W.v, g, &W.tri));
+            RSB_TRY(C.run(*P->tL1, VecIn{W.t3, nullptr, 0}, nullptr, W.v, P->tU, h));
         } else {
             RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{w, nullptr, 0}, W.t2, EPI_STORE, VecIn{}, g));
-            RSB_TRY(launch_trsv(ctx, *P->tL1T, VecIn{W.t2, nullptr, 0}, nullptr, W.t3, g, &W.tri));
-            RSB_TRY(launch_trsv(ctx, *P->tL1, r1, W.t3, W.v, g, &W.tri));
+            RSB_TRY(C.run(*P->tL1T, VecIn{W.t2, nullptr, 0}, nullptr, W.t3, P->tL1, W.v));
+            RSB_TRY(C.run(*P->tL1, r1, W.t3, W.v, P->tU, h));
         }
     } else {
-        RSB_TRY(launch_trsv(ctx, *P->tL1, r1, nullptr, W.v, g, &W.tri));
+        RSB_TRY(C.run(*P->tL1, r1, nullptr, W.v, P->tU, h));
     }
-    return launch_trsv(ctx, *P->tU, VecIn{W.v, nullptr, 0}, nullptr, h, g, &W.tri);
+    // the last solve refills the next application's first output
+    return C.run(*P->tU, VecIn{W.v, nullptr, 0}, nullptr, h, W.carry ? P->tL1 : nullptr, W.carry ? W.t1 : nullptr);
 }
 
 void pre_free(rsb_pre *P) {
@@ -656,7 +700,7 @@ int rsb_solver_create_on(rsb_ctx *ctx, rsb_mat *A, rsb_pre *pre, rsb_solver **ou
         set_error("pinned allocation failed");
         rc = RSB_ENOMEM;
     }
-    if (rc == RSB_OK && pre) rc = ws_alloc(ctx, pre, S->ws);
+    if (rc == RSB_OK && pre) rc = ws_alloc(ctx, pre, S->ws, /*carry=*/true);
     if (rc == RSB_OK) rc = cudaStreamSynchronize(ctx->stream) == cudaSuccess ? RSB_OK : RSB_ECUDA;
     if (rc != RSB_OK) {
         solver_free(S);

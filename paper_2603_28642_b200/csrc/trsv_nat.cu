@@ -92,7 +92,17 @@ __device__ __forceinline__ NatSlice nat_slice_load(const NatSrc &s, int n, const
 template <int MODE, int MINB, bool STATIC>
 __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, VecIn a, const double *c, double *x,
                                                           unsigned long long *ticket, int cap, unsigned max_backoff,
-                                                          unsigned min_backoff, Gate g) {
+                                                          unsigned min_backoff, Gate g, double *fill) {
+    if (fill) {
+        // this block's share of the sentinel fill of the chain's next output
+        // (TrsvChain): before the gate, so the vector is filled whatever the
+        // status says; the stores drain while the slices below wait on their
+        // dependencies
+        const int64_t per = (((int64_t)n + gridDim.x - 1) / gridDim.x + 31) & ~(int64_t)31;
+        const int64_t lo = blockIdx.x * per, hi = min((int64_t)n, lo + per);
+        const double sent = __longlong_as_double((long long)kSentinel);
+        for (int64_t i = lo + threadIdx.x; i < hi; i += kNatBlock) fill[i] = sent;
+    }
     if (STATIC) {
         if (*(volatile const unsigned long long *)ticket) return;  // the gate's snapshot
     } else if (gated(g)) {
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
 
 
 using NatKernel = void (*)(NatSrc, int, VecIn, const double *, double *, unsigned long long *, int, unsigned, unsigned,
-                           Gate);
+                           Gate, double *);
 
 // (A pipelined static-schedule variant -- a warp owning slices w, w + W, ... and
 // running three stages across them: pointers and right-hand side of s + 2W by
@@ -275,7 +285,8 @@ NatKernel nat_kernel(int mode, int minb, bool st) {
 
 size_t trsv_nat_smem(int mode, int cap) { return (size_t)kNatWarps * cap * nat_entry_bytes(mode); }
 
-int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g) {
+int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g,
+                    bool prefilled, double *fill_next) {
     const char *em = getenv("RSB_NAT_MINB");  // experiments
     const int minb = em ? atoi(em) : kNatMinBlocks;
     const char *es = getenv("RSB_NAT_STATIC");
@@ -299,7 +310,7 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
     const unsigned min_backoff = emb ? (unsigned)std::max(8, atoi(emb)) : kNatMinBackoffNs;
     const int64_t nsl = ((int64_t)T.n + 31) / 32;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * occ, (nsl + kNatWarps - 1) / kNatWarps));
-    RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
+    if (!prefilled) RSB_TRY(launch_fill(ctx, x, T.n, kSentinel, g));
     if (st) {
         k_nat_gate_snap<<<1, 1, 0, ctx->stream>>>(g, v.ticket);
         RSB_TRY_CUDA(cudaGetLastError());
@@ -313,10 +324,12 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g));
+        RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g,
+                                        fill_next));
         return RSB_OK;
     }
-    k<<<grid, kNatBlock, smem, ctx->stream>>>(T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g);
+    k<<<grid, kNatBlock, smem, ctx->stream>>>(T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g,
+                                              fill_next);
     return RSB_OK;
 }
 

@@ -133,3 +133,32 @@ def test_config4_structure_fixed_iterations_wide_dag():
     A, B = W.config4(seed=4, n=200_000, nrhs=1)
     S, na, f = _pipeline(A, True, 1.0, 0.0, 4)
     _check(S, B[0], na, f, "cg", 1e-300, 6, 4)
+
+
+@pytest.mark.parametrize("cg_iters", [1, 2, 3])
+def test_index_order_solve_chain_across_solves(cg_iters, monkeypatch):
+    """The index-order solves of one application fill each other's outputs
+    with the sentinel (TrsvChain, csrc/solver.cu), the last one refilling the
+    next application's first output.  One solver runs to convergence (its
+    gated tail must leave the chain intact), stops at max_iters, and is
+    started again with other right-hand sides, with standalone applications
+    (the preconditioner's own workspace) in between: all bit-identical to the
+    oracle, for 1 / 2 / 3 inner CG steps (odd steps use the second buffer)."""
+    from paper_2603_28642_b200 import device
+
+    monkeypatch.setenv("RSB_TRSV_ORDER", "natural")
+    device.clear_caches()
+    A, B = W.config4(seed=14, n=100_000, nrhs=3)
+    S, na, f = _pipeline(A, True, 1.0, 0.0, 14)
+    pre = P.build_preconditioner(f, s_mode=P.SMode("cg"), cg_iters=cg_iters)
+    op = O.OraclePreconditioner.from_reference(pre)
+    rng = np.random.default_rng(99)
+    n = S.ncols
+    for j, (delta, its) in enumerate(((1e-8, 60), (1e-300, 4), (1e-6, 60))):
+        x, rep = P.pcgls(S, B[j], pre, P.CglsConfig(norm_A=na, delta=delta, max_iters=its))
+        xo, repo = O.pcgls(S, B[j], op, na, delta=delta, max_iters=its)
+        assert np.array_equal(x, xo, equal_nan=True), f"solve {j}: iterate differs"
+        assert _same_report(rep, repo), f"solve {j}: report differs"
+        r1, r2 = rng.standard_normal(n), rng.standard_normal(S.nrows - n)
+        assert np.array_equal(pre.apply(r1, r2), op.apply(r1, r2), equal_nan=True), f"apply after solve {j} differs"
+    device.clear_caches()
