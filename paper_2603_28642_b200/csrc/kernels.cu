@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
     // ingest rate (~16 B/cycle against the 64 the chain could use), so half
     // the bytes is close to half the time; same products, same order
     // and its buffers hold twice the stages
-    const bool same = a_all == b_all;
+    const bool same = a_all == b_all && norm_stages > 0;
     const int nst = same ? norm_stages : kDotStages;
     const size_t sbuf = same ? kBuf : 2 * kBuf;  // doubles per stage
     const int64_t n32 = (n & ~(int64_t)15) & ~(int64_t)31;
@@ -606,29 +606,39 @@ __global__ void __launch_bounds__(32) k_dot_exact_staged(int64_t n_all, const do
         // shared-memory latency
         constexpr int G = 8;
         const int full_groups = steps / G;
-        double ra[G], rb[G];
-        if (full_groups > 0) {
+        // two register sets, ping-pong: the loads of group g + 1 / g + 2 are in
+        // flight while group g / g + 1 issues (pointer bumps only -- an index
+        // select in the address made ptxas park a whole group's loads right in
+        // front of their first use)
+        double a0[G], b0[G], a1[G], b1[G];
+        const double *pa = sa, *pb = sb;
+        auto ld = [&](double(&ra)[G], double(&rb)[G], const double *qa, const double *qb) {
 #pragma unroll
             for (int j = 0; j < G; ++j) {
-                ra[j] = sa[32 * j];
-                rb[j] = sb[32 * j];
+                ra[j] = qa[32 * j];
+                rb[j] = qb[32 * j];
             }
-        }
-        for (int gI = 0; gI < full_groups; ++gI) {
-            double na[G], nb[G];
-            const int nxt = (gI + 1 < full_groups) ? (gI + 1) * G : gI * G;  // last group: reload, unused
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                na[j] = sa[32 * (nxt + j)];
-                nb[j] = sb[32 * (nxt + j)];
-            }
+        };
+        auto mac = [&](const double(&ra)[G], const double(&rb)[G]) {
 #pragma unroll
             for (int j = 0; j < G; ++j) acc = fma(ra[j], rb[j], acc);
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-                ra[j] = na[j];
-                rb[j] = nb[j];
-            }
+        };
+        int gI = 0;
+        if (full_groups > 0) ld(a0, b0, pa, pb);
+        for (; gI + 3 <= full_groups; gI += 2) {
+            ld(a1, b1, pa + 32 * G, pb + 32 * G);
+            mac(a0, b0);
+            ld(a0, b0, pa + 64 * G, pb + 64 * G);
+            mac(a1, b1);
+            pa += 64 * G;
+            pb += 64 * G;
+        }
+        if (gI + 2 == full_groups) {
+            ld(a1, b1, pa + 32 * G, pb + 32 * G);
+            mac(a0, b0);
+            mac(a1, b1);
+        } else if (gI + 1 == full_groups) {
+            mac(a0, b0);
         }
         for (int k = full_groups * G; k < steps; ++k) acc = fma(sa[32 * k], sb[32 * k], acc);
         __syncwarp();
@@ -1391,7 +1401,7 @@ int launch_dot(rsb_ctx *ctx, int64_t n, VecIn a, VecIn b, double *out, int sqrt_
         const size_t smem = (size_t)kDotStages * 2 * (kDotChunk + 2) * 8 + 2 * kDotStages * 8;
         static const int norm_stages = [] {  // experiments: stages of the one-stream norm (2 .. 2 * kDotStages)
             const char *e = getenv("RSB_DOT_NORM_STAGES");
-            return e ? std::max(2, std::min(2 * kDotStages, atoi(e))) : 2 * kDotStages;
+            return e ? std::max(0, std::min(2 * kDotStages, atoi(e))) : 2 * kDotStages;  // 0: two streams
         }();
         k_dot_exact_staged<<<ch.T, 32, smem, ctx->stream>>>(n, a.p, b.p, out, sqrt_out, g, need, ch, norm_stages);
         return post_launch(ctx);
