@@ -81,6 +81,7 @@ struct ApplyWs {
     double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;            // s
     double *cg_a = nullptr, *cg_b = nullptr, *cg_c = nullptr;            // n
     double *cg_b2 = nullptr;  // n: cg_b of the odd inner-CG steps (a solve fills its successor's output, TrsvChain)
+    double *r1g = nullptr;    // n: r1 as the first solve gathered it, for the application's second solve with r1
     CgState *cg = nullptr;
     TriWs tri;
     // A solver's own workspace (only enqueue_apply touches it): t1, the first

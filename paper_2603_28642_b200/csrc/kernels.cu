@@ -1299,7 +1299,7 @@ int launch_trsv(rsb_ctx *ctx, const TriSched &T, VecIn a, const double *c, doubl
     } else if (T.wide && T.use_nat) {
         RSB_TRY_CUDA(cudaMemsetAsync(v.ticket, 0, sizeof(unsigned long long), ctx->stream));
         // sentinel fill unless the chain's previous solve did it, then the solve (counted below)
-        RSB_TRY(launch_trsv_nat(ctx, T, v, a, c, x, g, chain.prefilled, chain.fill_next));
+        RSB_TRY(launch_trsv_nat(ctx, T, v, a, c, x, g, chain.prefilled, chain.fill_next, chain.rhs_copy));
     } else if (T.wide && T.level_sync) {
         // level-synchronous cooperative solve (trsv_ls.cu), the default for wide DAGs
         RSB_TRY(launch_trsv_ls(ctx, T, v, a, c, x, reinterpret_cast<unsigned *>(v.ticket), g, 1, nullptr, 0));

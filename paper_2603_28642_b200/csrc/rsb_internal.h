@@ -419,7 +419,7 @@ constexpr int kNatMaxCap = 1024;
 // wrote it); fill_next: an n-vector this launch also fills with the sentinel
 // (the next solve's output), gate or no gate
 int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g,
-                    bool prefilled = false, double *fill_next = nullptr);
+                    bool prefilled = false, double *fill_next = nullptr, double *rhs_copy = nullptr);
 size_t trsv_nat_smem(int mode, int cap);
 int tri_setup_nat(rsb_mat *T, int kind, TriSched *S);
 TaskSrc tri_task_src(const rsb_mat *T, int kind);
@@ -483,6 +483,10 @@ int launch_spmv_t(rsb_ctx *ctx, const Compressed &At, VecIn y, double *z, int ep
 struct TrsvChain {
     bool prefilled = false;       // x already holds the sentinel
     double *fill_next = nullptr;  // n-vector to fill with the sentinel (nullptr: none)
+    // n-vector that receives the right-hand side a(row) as the solve reads it
+    // (a permuted gather paid once for two solves); only where
+    // trsv_wants_prefill(T) -- other variants ignore it
+    double *rhs_copy = nullptr;
 };
 inline bool trsv_wants_prefill(const TriSched &T) { 
     return T.n > 0 && !T.single_cta && !T.level_launch && !T.lsync && T.wide && T.use_nat;  // launch_trsv's dispatch

@@ -199,7 +199,7 @@ int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W, bool carry = false) {
     W.n = P->n;
     W.s = P->s;
     const size_t n8 = P->n * sizeof(double), s8 = P->s * sizeof(double);
-    for (double **q : {&W.t1, &W.t2, &W.t3, &W.v, &W.cg_a, &W.cg_b, &W.cg_c, &W.cg_b2})
+    for (double **q : {&W.t1, &W.t2, &W.t3, &W.v, &W.cg_a, &W.cg_b, &W.cg_c, &W.cg_b2, &W.r1g})
         RSB_TRY(dev_alloc(ctx, (void **)q, n8));
     for (double **q : {&W.u, &W.w, &W.cg_r, &W.cg_p, &W.cg_q}) RSB_TRY(dev_alloc(ctx, (void **)q, s8));
     RSB_TRY(dev_alloc(ctx, (void **)&W.cg, sizeof(CgState)));
@@ -218,7 +218,7 @@ int ws_alloc(rsb_ctx *ctx, const rsb_pre *P, ApplyWs &W, bool carry = false) {
 void ws_free(ApplyWs &W) {
     if (!W.ctx) return;
     const size_t n8 = W.n * sizeof(double), s8 = W.s * sizeof(double);
-    for (double *q : {W.t1, W.t2, W.t3, W.v, W.cg_a, W.cg_b, W.cg_c, W.cg_b2}) dev_free(W.ctx, q, n8);
+    for (double *q : {W.t1, W.t2, W.t3, W.v, W.cg_a, W.cg_b, W.cg_c, W.cg_b2, W.r1g}) dev_free(W.ctx, q, n8);
     for (double *q : {W.u, W.w, W.cg_r, W.cg_p, W.cg_q}) dev_free(W.ctx, q, s8);
     dev_free(W.ctx, W.cg, sizeof(CgState));
     tri_ws_free(W.ctx, W.tri);
@@ -233,8 +233,10 @@ struct SolveChain {
     ApplyWs &W;
     Gate g;
     double *ready;
-    int run(const TriSched &T, VecIn a, const double *c, double *x, const TriSched *next, double *next_x) {
+    int run(const TriSched &T, VecIn a, const double *c, double *x, const TriSched *next, double *next_x,
+            double *rhs_copy = nullptr) {
         TrsvChain ch;
+        ch.rhs_copy = rhs_copy;
         ch.prefilled = ready != nullptr && ready == x;
         ch.fill_next = (next && next_x && trsv_wants_prefill(*next)) ? next_x : nullptr;
         RSB_TRY(launch_trsv(ctx, T, a, c, x, g, &W.tri, ch));
@@ -308,11 +310,17 @@ int enqueue_apply(rsb_pre *P, ApplyWs &W, VecIn r1, VecIn r2, double *h, Gate g)
         const TriSched *back = expl ? P->tL1 : P->tL1T;
         double *back_x = expl ? W.v : W.t3;
         const bool cg = P->s_mode != RSB_S_DENSE && P->s_mode != RSB_S_IDENTITY;
+        VecIn r1_again = r1;
         // u = r2 - Y r1
         if (expl) {
             RSB_TRY(launch_spmv(ctx, P->Y->csr(), r1, W.u, EPI_SUB_FROM, r2, g));
         } else {
-            RSB_TRY(C.run(*P->tL1, r1, nullptr, W.t1, cg ? P->tL1T : back, cg ? W.cg_b : back_x));
+            // r1 arrives through the row permutation (a scattered gather of
+            // the m-vector r): the index-order solve writes what it gathered
+            // to r1g, and the application's second solve with r1 streams that
+            r1_again = (r1.g && trsv_wants_prefill(*P->tL1)) ? VecIn{W.r1g, nullptr, 0} : r1;
+            RSB_TRY(C.run(*P->tL1, r1, nullptr, W.t1, cg ? P->tL1T : back, cg ? W.cg_b : back_x,
+                          r1_again.p == W.r1g ? W.r1g : nullptr));
             RSB_TRY(launch_spmv(ctx, P->L2->csr(), VecIn{W.t1, nullptr, 0}, W.u, EPI_SUB_FROM, r2, g));
         }
         // w = solve_S(u)
@@ -331,7 +339,7 @@ int enqueue_apply(rsb_pre *P, ApplyWs &W, VecIn r1, VecIn r2, double *h, Gate g)
         } else {
             RSB_TRY(launch_spmv_t(ctx, P->L2->csc(), VecIn{w, nullptr, 0}, W.t2, EPI_STORE, VecIn{}, g));
             RSB_TRY(C.run(*P->tL1T, VecIn{W.t2, nullptr, 0}, nullptr, W.t3, P->tL1, W.v));
-            RSB_TRY(C.run(*P->tL1, r1, W.t3, W.v, P->tU, h));
+            RSB_TRY(C.run(*P->tL1, r1_again, W.t3, W.v, P->tU, h));
         }
     } else {
         RSB_TRY(C.run(*P->tL1, r1, nullptr, W.v, P->tU, h));

@@ -73,7 +73,7 @@ struct NatSlice {
 };
 
 __device__ __forceinline__ NatSlice nat_slice_load(const NatSrc &s, int n, const VecIn &a, const double *c, int w,
-                                                   int nsl, int lane) {
+                                                   int nsl, int lane, double *rhs_copy = nullptr) {
     NatSlice r{0, 0, 0.0};
     if (w >= nsl) return r;
     const int q = w * 32 + lane;
@@ -82,6 +82,7 @@ __device__ __forceinline__ NatSlice nat_slice_load(const NatSrc &s, int n, const
         r.elo = __ldg(s.ptr + t);
         r.ehi = __ldg(s.ptr + t + 1);
         r.acc = a.g ? a.p[a.g[t + a.off]] : a.p[t + a.off];
+        if (rhs_copy) rhs_copy[t] = r.acc;  // the gathered a(t), contiguous, for a later solve of the chain
         if (c) r.acc = __dadd_rn(r.acc, c[t]);
     } else {  // past the end (last slice only): an empty line at the span's edge
         r.elo = r.ehi = __ldg(s.ptr + (s.forward ? n : 0));
@@ -92,7 +93,8 @@ __device__ __forceinline__ NatSlice nat_slice_load(const NatSrc &s, int n, const
 template <int MODE, int MINB, bool STATIC>
 __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, VecIn a, const double *c, double *x,
                                                           unsigned long long *ticket, int cap, unsigned max_backoff,
-                                                          unsigned min_backoff, Gate g, double *fill) {
+                                                          unsigned min_backoff, Gate g, double *fill,
+                                                          double *rhs_copy) {
     if (fill) {
         // this block's share of the sentinel fill of the chain's next output
         // (TrsvChain): before the gate, so the vector is filled whatever the
@@ -119,15 +121,15 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
     const unsigned full = 0xffffffffu;
     const int wstride = gridDim.x * kNatWarps;
     int w = STATIC ? blockIdx.x * kNatWarps + warp : 0;
-    NatSlice nx = STATIC ? nat_slice_load(s, n, a, c, w, nsl, lane) : NatSlice{0, 0, 0.0};
+    NatSlice nx = STATIC ? nat_slice_load(s, n, a, c, w, nsl, lane, rhs_copy) : NatSlice{0, 0, 0.0};
     for (;; w += wstride) {
         if (!STATIC) {
             if (lane == 0) w = (int)atomicAdd(ticket, 1ull);
             w = __shfl_sync(full, w, 0);
         }
         if (w >= nsl) break;
-        const NatSlice cur = STATIC ? nx : nat_slice_load(s, n, a, c, w, nsl, lane);
-        if (STATIC) nx = nat_slice_load(s, n, a, c, w + wstride, nsl, lane);  // in flight during this slice
+        const NatSlice cur = STATIC ? nx : nat_slice_load(s, n, a, c, w, nsl, lane, rhs_copy);
+        if (STATIC) nx = nat_slice_load(s, n, a, c, w + wstride, nsl, lane, rhs_copy);  // in flight during this slice
         const int q = w * 32 + lane;
         const bool valid = q < n;
         const int t = s.forward ? q : n - 1 - q;
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(kNatBlock, MINB) k_trsv_nat(NatSrc s, int n, V
 
 
 using NatKernel = void (*)(NatSrc, int, VecIn, const double *, double *, unsigned long long *, int, unsigned, unsigned,
-                           Gate, double *);
+                           Gate, double *, double *);
 
 // (A pipelined static-schedule variant -- a warp owning slices w, w + W, ... and
 // running three stages across them: pointers and right-hand side of s + 2W by
@@ -286,7 +288,7 @@ NatKernel nat_kernel(int mode, int minb, bool st) {
 size_t trsv_nat_smem(int mode, int cap) { return (size_t)kNatWarps * cap * nat_entry_bytes(mode); }
 
 int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, const double *c, double *x, Gate g,
-                    bool prefilled, double *fill_next) {
+                    bool prefilled, double *fill_next, double *rhs_copy) {
     const char *em = getenv("RSB_NAT_MINB");  // experiments
     const int minb = em ? atoi(em) : kNatMinBlocks;
     const char *es = getenv("RSB_NAT_STATIC");
@@ -325,11 +327,11 @@ int launch_trsv_nat(rsb_ctx *ctx, const TriSched &T, const TriDev &v, VecIn a, c
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         RSB_TRY_CUDA(cudaLaunchKernelEx(&cfg, k, T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g,
-                                        fill_next));
+                                        fill_next, rhs_copy));
         return RSB_OK;
     }
     k<<<grid, kNatBlock, smem, ctx->stream>>>(T.nat, T.n, a, c, x, v.ticket, T.nat_cap, max_backoff, min_backoff, g,
-                                              fill_next);
+                                              fill_next, rhs_copy);
     return RSB_OK;
 }
 
